@@ -1,0 +1,370 @@
+// rf_api.cpp — C ABI of include/rf_offpolicy.h: host-side validation mirroring the
+// reference's throw sites (losses.cpp:32-39,140-174), kernel selection, cluster
+// geometry, and the host-buffer streaming entry point.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "rf_kernels.h"
+#include "rf_offpolicy.h"
+
+using rf::KParams;
+
+namespace {
+
+thread_local int32_t g_last_launches = 0;
+
+bool is_aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+struct RingGeometry {
+    bool ok = false;
+    int cs = 1;
+    int row_vecs = 0, slice_vecs = 0, nchunks = 0, nslots = 0;
+    size_t smem = 0;
+};
+
+int max_optin_smem() {
+    static int v = -1;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (v < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 0;
+    }
+    return v;
+}
+
+size_t dtype_size(int32_t d) { return d == RF_DTYPE_BF16 ? 2 : (d == RF_DTYPE_F32 ? 4 : 8); }
+
+// The ring kernel needs every logits row (and dlogits row) to start on a 16-byte
+// boundary with its 16-byte-padded length inside the row stride.
+RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
+    RingGeometry g;
+    const size_t es = dtype_size(b->logits_dtype), os = dtype_size(o->dlogits_dtype);
+    const int epv = static_cast<int>(16 / es);
+    g.row_vecs = (b->vocab + epv - 1) / epv;
+    if (!is_aligned(b->logits, 16) || (b->logits_row_stride * static_cast<int64_t>(es)) % 16 != 0) return g;
+    if (b->logits_row_stride < static_cast<int64_t>(g.row_vecs) * epv) return g;
+    if (o->dlogits == nullptr || !is_aligned(o->dlogits, 16)) return g;
+    if ((o->dlogits_row_stride * static_cast<int64_t>(os)) % 16 != 0) return g;
+    if (o->dlogits_row_stride < static_cast<int64_t>(g.row_vecs) * epv) return g;
+    const int maxsmem = max_optin_smem();
+    const int nslots_max =
+        static_cast<int>((static_cast<size_t>(maxsmem) - rf::kRingTailBytes - 16) / (rf::kRingSlotBytes + 16));
+    for (int cs = 1; cs <= 8; cs *= 2) {
+        const int slice = (g.row_vecs + cs - 1) / cs;
+        if (cs > 1 && slice * (cs - 1) >= g.row_vecs) break;  // every rank must own >= 1 vector
+        const int nchunks = (slice + rf::kRingChunkVecs - 1) / rf::kRingChunkVecs;
+        if (nchunks <= nslots_max - 1) {
+            g.cs = cs;
+            g.slice_vecs = slice;
+            g.nchunks = nchunks;
+            g.nslots = nslots_max;
+            g.smem = static_cast<size_t>(g.nslots) * (rf::kRingSlotBytes + 16) + 16 + rf::kRingTailBytes;
+            g.ok = true;
+            return g;
+        }
+    }
+    return g;
+}
+
+int ring_clusters(bool ib, bool ob, int cs, size_t smem) {
+    struct Key {
+        bool ib, ob;
+        int cs;
+        size_t smem;
+        int val;
+    };
+    static std::vector<Key> cache;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Key& k : cache)
+        if (k.ib == ib && k.ob == ob && k.cs == cs && k.smem == smem) return k.val;
+    int n = 0;
+    if (rf::ring_max_clusters(ib, ob, cs, smem, &n) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        n = sms / cs;
+    }
+    cache.push_back({ib, ob, cs, smem, n});
+    return n;
+}
+
+int generic_grid(int64_t T) { return static_cast<int>(std::min<int64_t>(T, rf::kGenericMaxGrid)); }
+
+int64_t partial_rows(const rf_batch* b) { return std::max<int64_t>(rf::kGenericMaxGrid, b->num_seqs); }
+
+struct WsLayout {
+    double* partials = nullptr;
+    double *lse = nullptr, *lp = nullptr, *coef = nullptr, *klx = nullptr, *lseq = nullptr;
+    size_t bytes = 0;
+};
+
+WsLayout ws_layout(const rf_loss_config* c, const rf_batch* b, void* base) {
+    WsLayout w;
+    uint8_t* p = static_cast<uint8_t*>(base);
+    size_t off = 0;
+    auto take = [&](size_t n) {
+        void* r = p ? p + off : nullptr;
+        off += (n + 255) & ~size_t(255);
+        return static_cast<double*>(r);
+    };
+    w.partials = take(static_cast<size_t>(partial_rows(b)) * RF_NUM_SCALARS * sizeof(double));
+    if (c->aggregation == RF_SEQUENCE_PRODUCT) {
+        const size_t T = static_cast<size_t>(b->num_tokens);
+        w.lse = take(T * 8);
+        w.lp = take(T * 8);
+        w.coef = take(T * 8);
+        w.klx = take(T * 8);
+        w.lseq = take(T * 8);
+    }
+    w.bytes = off;
+    return w;
+}
+
+rf_status check_cuda(cudaError_t e) { return e == cudaSuccess ? RF_OK : RF_ERR_CUDA; }
+
+}  // namespace
+
+extern "C" {
+
+void rf_loss_config_default(rf_loss_config* c) {
+    c->variant = RF_PPO;
+    c->aggregation = RF_TOKEN_MEAN;
+    c->clip_eps = 0.2;
+    c->eps_low = 0.2;
+    c->eps_high = 0.2;
+    c->trunc_cap = 5.0;
+    c->kl_weight = 0.0;
+    c->w_plus = 1.0;
+    c->w_minus = 1.0;
+    c->engine_mismatch_cap = 0.0;
+}
+
+rf_status rf_loss_config_validate(const rf_loss_config* c) {
+    if (!c) return RF_ERR_INVALID_ARGUMENT;
+    if (!(c->clip_eps > 0.0 && c->clip_eps < 1.0)) return RF_ERR_CLIP_EPS;
+    if (c->eps_low < 0.0 || c->eps_high < 0.0) return RF_ERR_EPS_LOW_HIGH;
+    if (c->trunc_cap <= 0.0) return RF_ERR_TRUNC_CAP;
+    if (c->kl_weight < 0.0) return RF_ERR_KL_WEIGHT;
+    if (c->w_plus < 0.0 || c->w_minus < 0.0) return RF_ERR_TOPR_WEIGHTS;
+    if (c->engine_mismatch_cap < 0.0) return RF_ERR_MISMATCH_CAP;
+    if (c->variant < RF_PPO || c->variant > RF_NAIVE_IS) return RF_ERR_UNKNOWN_VARIANT;
+    if (c->aggregation != RF_TOKEN_MEAN && c->aggregation != RF_SEQUENCE_PRODUCT) return RF_ERR_INVALID_ARGUMENT;
+    return RF_OK;
+}
+
+const char* rf_loss_variant_name(int32_t v) {
+    switch (v) {
+        case RF_PPO: return "ppo";
+        case RF_DECOUPLED_PPO: return "decoupled_ppo";
+        case RF_TIS: return "tis";
+        case RF_CISPO: return "cispo";
+        case RF_TOPR: return "topr";
+        case RF_GRPO: return "grpo";
+        case RF_NAIVE_IS: return "naive_is";
+    }
+    return "unknown";
+}
+
+rf_status rf_loss_variant_from_name(const char* name, int32_t* out) {
+    if (!name || !out) return RF_ERR_INVALID_ARGUMENT;
+    for (int32_t v = RF_PPO; v <= RF_NAIVE_IS; ++v) {
+        if (std::strcmp(name, rf_loss_variant_name(v)) == 0) {
+            *out = v;
+            return RF_OK;
+        }
+    }
+    return RF_ERR_UNKNOWN_VARIANT;
+}
+
+const char* rf_status_string(rf_status s) {
+    switch (s) {
+        case RF_OK: return "ok";
+        case RF_ERR_CLIP_EPS: return "LossConfig: clip_eps must be in (0,1)";
+        case RF_ERR_EPS_LOW_HIGH: return "LossConfig: eps_low/eps_high must be >= 0";
+        case RF_ERR_TRUNC_CAP: return "LossConfig: trunc_cap must be > 0";
+        case RF_ERR_KL_WEIGHT: return "LossConfig: kl_weight must be >= 0";
+        case RF_ERR_TOPR_WEIGHTS: return "LossConfig: TOPR weights must be >= 0";
+        case RF_ERR_MISMATCH_CAP: return "LossConfig: engine_mismatch_cap must be >= 0";
+        case RF_ERR_EMPTY_BATCH: return "loss_and_grad: empty batch";
+        case RF_ERR_MISSING_PROX: return "loss_and_grad: decoupled_ppo requires a proximal policy";
+        case RF_ERR_MISSING_REF: return "loss_and_grad: grpo with kl_weight > 0 requires a reference policy";
+        case RF_ERR_EMPTY_TRAJECTORY: return "loss_and_grad: empty trajectory";
+        case RF_ERR_MISSING_ENGINE_LOGP: return "loss_and_grad: engine log-probs missing for mismatch correction";
+        case RF_ERR_NONFINITE_RATIO: return "loss_and_grad: non-finite ratio";
+        case RF_ERR_GROUP_TOO_SMALL: return "grpo_advantages: group size must be >= 2";
+        case RF_ERR_UNKNOWN_VARIANT: return "unknown loss variant";
+        case RF_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case RF_ERR_UNSUPPORTED_LAYOUT: return "unsupported layout";
+        case RF_ERR_TOKEN_OUT_OF_RANGE: return "token id out of range";
+        case RF_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+        case RF_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+size_t rf_workspace_bytes(const rf_loss_config* c, const rf_batch* b) {
+    if (!c || !b) return 0;
+    return ws_layout(c, b, nullptr).bytes;
+}
+
+int32_t rf_last_launch_count(void) { return g_last_launches; }
+
+rf_status rf_zero_scalars(rf_outputs* o, void* stream) {
+    if (!o || !o->scalars || !o->device_status) return RF_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(o->scalars, 0, RF_NUM_SCALARS * sizeof(double), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(o->device_status, 0, sizeof(int32_t), st);
+    return check_cuda(e);
+}
+
+rf_status rf_grpo_advantages(const rf_batch* b, rf_outputs* o, void* stream) {
+    if (!b || !o) return RF_ERR_INVALID_ARGUMENT;
+    if (b->num_groups <= 0) return RF_ERR_EMPTY_BATCH;
+    if (!b->rewards || !b->group_offsets || !o->advantages_out || !o->group_degenerate || !o->device_status)
+        return RF_ERR_INVALID_ARGUMENT;
+    g_last_launches = 1;
+    return check_cuda(rf::launch_grpo(b->rewards, b->group_offsets, b->num_groups, o->advantages_out,
+                                      o->group_degenerate, o->device_status, static_cast<cudaStream_t>(stream)));
+}
+
+rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_outputs* o, void* stream,
+                              int32_t kernel) {
+    g_last_launches = 0;
+    if (!c || !b || !o) return RF_ERR_INVALID_ARGUMENT;
+    rf_status st = rf_loss_config_validate(c);
+    if (st != RF_OK) return st;
+    if (b->num_tokens <= 0 || b->num_seqs <= 0) return RF_ERR_EMPTY_BATCH;            // losses.cpp:140
+    const bool needs_prox = c->variant == RF_DECOUPLED_PPO;
+    const bool needs_ref = c->variant == RF_GRPO && c->kl_weight > 0.0;
+    if (needs_prox && !b->prox_logp) return RF_ERR_MISSING_PROX;                       // losses.cpp:142-144
+    if (needs_ref && !b->ref_logits) return RF_ERR_MISSING_REF;                        // losses.cpp:145-148
+    if (c->engine_mismatch_cap > 0.0 && !b->engine_logp) return RF_ERR_MISSING_ENGINE_LOGP;  // losses.cpp:173
+    if (!b->logits || !b->token_ids || !b->seq_of_token || !b->seq_offsets || !b->advantages || !b->behavior_logp)
+        return RF_ERR_INVALID_ARGUMENT;
+    if (!o->scalars || !o->device_status) return RF_ERR_INVALID_ARGUMENT;
+    if (b->vocab < 2) return RF_ERR_INVALID_ARGUMENT;
+    if (b->logits_dtype != RF_DTYPE_BF16 && b->logits_dtype != RF_DTYPE_F32) return RF_ERR_INVALID_ARGUMENT;
+    if (o->dlogits && o->dlogits_dtype != RF_DTYPE_BF16 && o->dlogits_dtype != RF_DTYPE_F32)
+        return RF_ERR_INVALID_ARGUMENT;
+    if (b->logp_dtype != RF_DTYPE_F32 && b->logp_dtype != RF_DTYPE_F64) return RF_ERR_INVALID_ARGUMENT;
+    if (b->normalization == RF_NORM_SEQ_THEN_BATCH && b->global_num_seqs <= 0) return RF_ERR_INVALID_ARGUMENT;
+    if (b->normalization == RF_NORM_GLOBAL_TOKEN && b->global_num_tokens <= 0) return RF_ERR_INVALID_ARGUMENT;
+    if (b->normalization != RF_NORM_SEQ_THEN_BATCH && b->normalization != RF_NORM_GLOBAL_TOKEN)
+        return RF_ERR_INVALID_ARGUMENT;
+    if (b->logits_row_stride < b->vocab) return RF_ERR_INVALID_ARGUMENT;
+    if (needs_ref && b->ref_row_stride < b->vocab) return RF_ERR_INVALID_ARGUMENT;
+    if (o->dlogits && o->dlogits_row_stride < b->vocab) return RF_ERR_INVALID_ARGUMENT;
+
+    const WsLayout ws = ws_layout(c, b, o->workspace);
+    if (!o->workspace || o->workspace_bytes < ws.bytes) return RF_ERR_WORKSPACE_TOO_SMALL;
+
+    KParams p{};
+    p.variant = c->variant;
+    p.aggregation = c->aggregation;
+    p.clip_eps = c->clip_eps;
+    p.eps_low = c->eps_low;
+    p.eps_high = c->eps_high;
+    p.trunc_cap = c->trunc_cap;
+    p.kl_weight = c->kl_weight;
+    p.w_plus = c->w_plus;
+    p.w_minus = c->w_minus;
+    p.mismatch_cap = c->engine_mismatch_cap;
+    p.T = b->num_tokens;
+    p.V = b->vocab;
+    p.logp_f64 = b->logp_dtype == RF_DTYPE_F64 ? 1 : 0;
+    p.logits = b->logits;
+    p.row_stride = b->logits_row_stride;
+    p.ref_logits = needs_ref ? b->ref_logits : nullptr;
+    p.ref_row_stride = b->ref_row_stride;
+    p.row_of_token = b->row_of_token;
+    p.token_ids = b->token_ids;
+    p.seq_of_token = b->seq_of_token;
+    p.seq_offsets = b->seq_offsets;
+    p.advantages = b->advantages;
+    p.behavior_logp = b->behavior_logp;
+    p.prox_logp = b->prox_logp;
+    p.engine_logp = b->engine_logp;
+    p.normalization = b->normalization;
+    p.inv_n = b->global_num_seqs > 0 ? 1.0 / static_cast<double>(b->global_num_seqs) : 0.0;
+    p.inv_t = b->global_num_tokens > 0 ? 1.0 / static_cast<double>(b->global_num_tokens) : 0.0;
+    p.grad_sign = b->grad_sign;
+    p.dlogits = o->dlogits;
+    p.dl_stride = o->dlogits_row_stride;
+    p.token_logp = o->token_logp;
+    p.token_ratio = o->token_ratio;
+    p.token_coef = o->token_coef;
+    p.token_loss = o->token_loss;
+    p.token_flags = o->token_flags;
+    p.status = o->device_status;
+    p.partials = ws.partials;
+    p.mode = 0;
+
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool ib = b->logits_dtype == RF_DTYPE_BF16;
+    const bool ob = o->dlogits_dtype == RF_DTYPE_BF16;
+    int64_t nparts = 0;
+
+    if (c->aggregation == RF_SEQUENCE_PRODUCT) {
+        // Two passes over the logits (losses.cpp:180-259): the sequence weights
+        // need every token's log-prob first.
+        p.tok_lse = ws.lse;
+        p.tok_klx = ws.klx;
+        p.tok_lseq = ws.lseq;
+        p.token_logp = o->token_logp ? o->token_logp : ws.lp;
+        const int grid = generic_grid(b->num_tokens);
+        p.mode = 1;
+        if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
+        if (rf::launch_seq(p, 0, b->num_seqs, ws.coef, s) != cudaSuccess) return RF_ERR_CUDA;
+        if (o->token_coef)
+            if (cudaMemcpyAsync(o->token_coef, ws.coef, static_cast<size_t>(b->num_tokens) * 8,
+                                cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+                return RF_ERR_CUDA;
+        nparts = b->num_seqs;
+        g_last_launches = 2;
+        if (o->dlogits) {
+            KParams q = p;
+            q.mode = 2;
+            q.token_coef = ws.coef;
+            if (rf::launch_generic(q, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
+            g_last_launches += 1;
+        }
+    } else {
+        RingGeometry g;
+        if (kernel != RF_KERNEL_GENERIC && !needs_ref) g = ring_geometry(b, o);
+        if (kernel == RF_KERNEL_RING && !g.ok) return RF_ERR_UNSUPPORTED_LAYOUT;
+        if (g.ok) {
+            p.slice_vecs = g.slice_vecs;
+            p.row_vecs = g.row_vecs;
+            p.nchunks = g.nchunks;
+            p.nslots = g.nslots;
+            const int maxc = ring_clusters(ib, ob, g.cs, g.smem);
+            const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
+            if (rf::launch_ring(p, ib, ob, g.cs, ncl, g.smem, s) != cudaSuccess) return RF_ERR_CUDA;
+            nparts = ncl;
+        } else {
+            const int grid = generic_grid(b->num_tokens);
+            if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
+            nparts = grid;
+        }
+        g_last_launches = 1;
+    }
+    if (rf::launch_finalize(ws.partials, nparts, o->scalars, s) != cudaSuccess) return RF_ERR_CUDA;
+    g_last_launches += 1;
+    return RF_OK;
+}
+
+rf_status rf_loss_and_grad(const rf_loss_config* c, const rf_batch* b, rf_outputs* o, void* stream) {
+    return rf_loss_and_grad_ex(c, b, o, stream, RF_KERNEL_AUTO);
+}
+
+}  // extern "C"
