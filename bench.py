@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""Benchmark: fused off-policy loss + dlogits tokens/s and % HBM roofline on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+One step = the hot path over one synthetic long-tail rollout batch (BASELINE.json
+configs; default C2 = decoupled PPO, Qwen3 vocab 151,936, 256 prompts x 8
+responses per GPU, max len 8k, async ratio 2):
+  K1 GRPO group advantages -> K2 fused log-softmax/gather + ratio + surrogate +
+  bf16 dlogits, streamed in token chunks from a device logits pool (rows indexed
+  by row_of_token; pool and dlogits buffers far exceed L2) -> K3 scalar reduce ->
+  (N > 1) one NCCL all-reduce of the fp64 loss scalars.
+Whole GRPO groups are LPT-sharded across ranks (weak scaling: each rank owns a
+C2-sized shard of an N x C2 global batch).  Timing: CUDA events on the launching
+stream, barrier + synchronize on both sides, max over ranks.
+
+--impl reference times the reference's own CPU implementation (rlsim::loss_and_grad
+compiled from /root/reference into oracle/_ref, one length-1 trajectory per token)
+on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "loss+dlogits tokens/sec and % HBM roofline at 1/2/4/8 B200 vs CPU ref"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--prompts", type=int, default=None, help="prompts per rank (default: the config's)")
+    ap.add_argument("--chunk-tokens", type=int, default=65536)
+    ap.add_argument("--pool-gb", type=float, default=48.0)
+    ap.add_argument("--kernel", default="auto", choices=["auto", "ring", "generic"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-tokens", type=int, default=8192)
+    ap.add_argument("--cpu-rows", type=int, default=0, help="reference sample rows (0 = auto)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def traffic_per_token(vocab: int):
+    """dram read+write bytes per token of the ring kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ring_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(str(vocab), {}).get("dram_bytes_per_token")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref): rlsim::loss_and_grad on mapping-A rows
+# ---------------------------------------------------------------------------
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_sample(wl, rows, variant, seed=42):
+    """A bounded, seeded sample of the same workload on the host: `rows` token rows
+    (bf16 logits as fp64), tokens, advantages, behaviour/prox/engine log-probs."""
+    import numpy as np
+
+    from paper_2510_11345_b200 import synth as S
+
+    rb = S.make_rank_batch(wl, 0, 1, seed)
+    rng = np.random.default_rng(seed)
+    V = wl.vocab
+    x = rng.normal(0.0, 2.0, (rows, V)).astype(np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    x = (((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)).view(np.float32).astype(np.float64)
+    m = x.max(axis=1, keepdims=True)
+    lse = (m + np.log(np.exp(x - m).sum(axis=1, keepdims=True)))[:, 0]
+    tok = np.empty(rows, dtype=np.int32)
+    for r0 in range(0, rows, 256):  # Gumbel-max sampling, chunked to bound host memory
+        r1 = min(rows, r0 + 256)
+        tok[r0:r1] = np.argmax(x[r0:r1] + rng.gumbel(size=(r1 - r0, V)), axis=1)
+    lp = x[np.arange(rows), tok] - lse
+    seq = np.repeat(np.arange(len(rb.lengths)), rb.lengths)[:rows]
+    s = rb.stale[seq]
+    delta = rng.normal(0.0, 1.0, rows) * 0.05 * np.sqrt(s)
+    beh = lp - delta
+    prox = lp - delta / 2
+    eng = beh - rng.normal(0.0, 0.01, rows)
+    adv = np.zeros(len(rb.lengths))
+    G = rb.group
+    for gi in range(len(rb.lengths) // G):
+        r = rb.rewards[gi * G:(gi + 1) * G]
+        mean = r.sum() / G
+        sd = np.sqrt(((r - mean) ** 2).sum() / G)
+        if sd >= 1e-8:
+            adv[gi * G:(gi + 1) * G] = (r - mean) / sd
+    return x, tok, adv[seq], beh, prox, eng
+
+
+def prepare_reference(wl, variant, rows):
+    """Sample + the prox ToyPolicy table the reference needs (setup, untimed)."""
+    import oracle as O
+
+    x, tok, adv, beh, prox, eng = reference_sample(wl, rows, variant)
+    prox_tab = O.ref_build_prox_table(x, tok, prox) if variant == "decoupled_ppo" else None
+    return (x, tok, adv, beh, prox_tab)
+
+
+def run_reference_once(prep, variant, threads, reps=1):
+    """Wall seconds of rlsim::loss_and_grad over the prepared rows (oracle/_ref)."""
+    import oracle as O
+    from tests.cases import config
+
+    x, tok, adv, beh, prox_tab = prep
+    secs, _ = O.ref_bench_mapping_a(config(variant), x, tok, adv, beh, prox_logits=prox_tab, engine_logp=None,
+                                    threads=threads, reps=reps)
+    return secs
+
+
+def default_cpu_rows(wl, threads):
+    per_core = 96 if wl.vocab > 100000 else 400
+    return int(min(max(per_core * threads, 128), 2048 if wl.vocab > 100000 else 8192))
+
+
+def cpu_baseline(wl, variant, rows):
+    threads = host_threads()
+    rows = rows or default_cpu_rows(wl, threads)
+    secs = run_reference_once(prepare_reference(wl, variant, rows), variant, threads)
+    return {"value": rows / secs, "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "sample": f"{rows} token rows of {wl.name} (V={wl.vocab}, {variant}, mapping A: one length-1 "
+                      f"trajectory per token), rlsim::loss_and_grad from oracle/_ref on {threads} host threads "
+                      f"(one shard each), {secs:.2f} s wall"}
+
+
+def impl_reference(args, wl, variant):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = host_threads()
+    rows = args.cpu_rows or default_cpu_rows(wl, threads)
+    prep = prepare_reference(wl, variant, rows)
+    for _ in range(args.warmup):
+        run_reference_once(prep, variant, threads)
+    times = [run_reference_once(prep, variant, threads) for _ in range(args.steps)]
+    mean = sum(times) / len(times)
+    value = rows / mean
+    sample = (f"{rows} token rows of {wl.name} per step (V={wl.vocab}, {variant}, mapping A), "
+              f"rlsim::loss_and_grad from oracle/_ref on {threads} host threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.description, "variant": variant, "vocab": wl.vocab, "sample_rows": rows},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1):
+    """The reference-facing C-ABI call with HOST buffers (rf_loss_and_grad_host):
+    pinned host logits rows in, pinned host dlogits + per-token outputs + scalars
+    out; every H2D/D2H copy is inside the timed region."""
+    import ctypes
+
+    import torch
+
+    from paper_2510_11345_b200 import _abi
+    from paper_2510_11345_b200 import losses as L
+    from tests.cases import config
+
+    T = min(tokens, dw.T)
+    # whole sequences
+    offs = dw.seq_offsets.cpu()
+    n_seq = int(torch.searchsorted(offs, torch.tensor([T]), right=True)[0]) - 1
+    n_seq = max(n_seq, 1)
+    T = int(offs[n_seq])
+    V = dw.vocab
+    rows = dw.row_of_token[:T].long()
+    h_logits = torch.empty(T, V, dtype=torch.bfloat16, pin_memory=True)
+    h_logits.copy_(dw.pool[rows].cpu())
+    h_dl = torch.empty(T, V, dtype=torch.bfloat16, pin_memory=True)
+
+    def pin(t):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t.cpu())
+        return h
+
+    h_tok = pin(dw.token_ids[:T])
+    h_seq = pin(L.seq_of_token_from_offsets(dw.seq_offsets[: n_seq + 1]))
+    h_offs = pin(dw.seq_offsets[: n_seq + 1])
+    h_adv = pin(dw.advantages[:n_seq])
+    h_b = pin(dw.behavior_logp[:T])
+    h_q = pin(dw.prox_logp[:T])
+    h_e = pin(dw.engine_logp[:T])
+    outs = {k: torch.empty(T, dtype=torch.float64, pin_memory=True) for k in ["lp", "ratio", "coef", "loss"]}
+    h_flags = torch.empty(T, dtype=torch.uint8, pin_memory=True)
+    h_scal = torch.zeros(_abi.RF_NUM_SCALARS, dtype=torch.float64, pin_memory=True)
+    h_status = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+    cfg = config(variant).to_c()
+    b = _abi.rf_batch()
+    b.num_tokens, b.num_seqs, b.vocab = T, n_seq, V
+    b.logits_dtype, b.logits, b.logits_row_stride = _abi.RF_DTYPE_BF16, h_logits.data_ptr(), V
+    b.token_ids, b.seq_of_token, b.seq_offsets = h_tok.data_ptr(), h_seq.data_ptr(), h_offs.data_ptr()
+    b.advantages = h_adv.data_ptr()
+    b.logp_dtype, b.normalization = _abi.RF_DTYPE_F32, _abi.RF_NORM_GLOBAL_TOKEN
+    b.behavior_logp, b.prox_logp, b.engine_logp = h_b.data_ptr(), h_q.data_ptr(), h_e.data_ptr()
+    b.global_num_seqs, b.global_num_tokens, b.grad_sign = n_seq, T, 1.0
+    o = _abi.rf_outputs()
+    o.dlogits, o.dlogits_dtype, o.dlogits_row_stride = h_dl.data_ptr(), _abi.RF_DTYPE_BF16, V
+    o.token_logp, o.token_ratio = outs["lp"].data_ptr(), outs["ratio"].data_ptr()
+    o.token_coef, o.token_loss, o.token_flags = outs["coef"].data_ptr(), outs["loss"].data_ptr(), h_flags.data_ptr()
+    o.scalars, o.device_status = h_scal.data_ptr(), h_status.data_ptr()
+    lib = _abi.load_library()
+    dev = torch.cuda.current_device()
+    chunk = 2048
+    for _ in range(warmup):
+        st = lib.rf_loss_and_grad_host(ctypes.byref(cfg), ctypes.byref(b), ctypes.byref(o), dev, chunk)
+        assert st == 0, L.status_string(st)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        st = lib.rf_loss_and_grad_host(ctypes.byref(cfg), ctypes.byref(b), ctypes.byref(o), dev, chunk)
+        ts.append(time.perf_counter() - t0)
+        assert st == 0, L.status_string(st)
+    t = statistics.median(ts)
+    h2d = T * V * 2 + T * (4 + 4 + 4 * 3) + (n_seq + 1) * 8 + n_seq * 8
+    d2h = T * V * 2 + T * (8 * 4 + 1) + _abi.RF_NUM_SCALARS * 8 + 4
+    return {"value": T / t, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "sample": f"first {T} tokens ({n_seq} whole sequences) of this rank's batch per step, "
+                      f"rf_loss_and_grad_host (C ABI, pinned host buffers, {chunk}-token chunks "
+                      f"double-buffered over H2D/compute/D2H streams), median of {steps} wall-clock steps"}
+
+
+def impl_ours(args, wl, variant):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_11345_b200 as rf
+    from paper_2510_11345_b200 import losses as L
+    from paper_2510_11345_b200 import synth as S
+    from tests.cases import config
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    rb = S.make_rank_batch(wl, rank, world, 42, args.prompts)
+    dw = S.DeviceWorkload(rb, wl.vocab, pool_gb=args.pool_gb, device=dev, seed=42 + rank)
+    cfg = config(variant)
+    pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_offsets,
+                       advantages=dw.advantages, behavior_logp=dw.behavior_logp, row_of_token=dw.row_of_token,
+                       prox_logp=dw.prox_logp, engine_logp=dw.engine_logp, rewards=dw.rewards,
+                       group_offsets=dw.group_offsets, normalization=L.Normalization.global_token,
+                       global_num_seqs=rb.global_seqs, global_num_tokens=rb.global_tokens)
+    chunk = min(args.chunk_tokens, dw.T)
+    op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=chunk, kernel=args.kernel)
+    stream = torch.cuda.current_stream()
+    chunks = [(t0, min(dw.T, t0 + chunk)) for t0 in range(0, dw.T, chunk)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in chunks]
+
+    def step(record=False):
+        adv, _ = rf.grpo_advantages(pb.rewards, pb.group_offsets, stream)
+        pb.advantages = adv
+        op.zero(stream)
+        for i, (t0, t1) in enumerate(chunks):
+            if record:
+                ev[i][0].record(stream)
+            op.run(pb, t0, t1, stream)
+            if record:
+                ev[i][1].record(stream)
+        if world > 1:
+            dist.all_reduce(op.scalars)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard on the benchmark data: device status clean
+    assert int(op.status.item()) == 0, "device status set during warm-up"
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern_ms = 0.0
+    launches_before = op.launches
+    start.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+        # per-chunk kernel time (ring + finalize) accumulated after each step
+    stop.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_total = start.elapsed_time(stop)
+    # ring-kernel time over the last step's chunks (events reused per step)
+    for a, b2 in ev:
+        kern_ms += a.elapsed_time(b2)
+    launches = (op.launches - launches_before) + args.steps  # + one K1 per step
+    t_local = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_step = float(t_local[0]) / args.steps
+    tokens_global = rb.global_tokens
+    value = tokens_global / (ms_step / 1e3)
+
+    peak, peak_kind = load_peaks()
+    bytes_tok = 4 * wl.vocab
+    # achieved bandwidth of the dominant kernel: algorithmic bytes / kernel time (last step)
+    achieved = dw.T * bytes_tok / (kern_ms / 1e3) / 1e9
+    tpt = traffic_per_token(wl.vocab)
+    launch_tokens = chunks[0][1] - chunks[0][0]
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None if tpt is None else int(tpt * launch_tokens),
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, torch bf16 copy)" if peak_kind == "measured"
+            else "fallback 6.65 TB/s (B200_PROFILING.md)",
+            "kernel": "ring_kernel (K2, incl. its K3 finalize launch)",
+            "algorithmic_bytes_per_token": bytes_tok, "tokens_per_launch": launch_tokens,
+            "kernel_ms_per_step": round(kern_ms, 3)}
+
+    line = None
+    if rank == 0:
+        e2e = None
+        if not args.no_e2e:
+            try:
+                e2e = e2e_host_api(wl, variant, dw, args.e2e_tokens)
+            except Exception as exc:  # report, do not hide
+                e2e = {"value": None, "unit": "tokens/s", "error": repr(exc)}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(wl, variant, args.cpu_rows)
+            except Exception as exc:
+                cpu = {"value": None, "error": repr(exc)}
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": wl.description, "variant": variant, "vocab": wl.vocab,
+                       "prompts_per_gpu": args.prompts or wl.prompts, "group": wl.group, "max_len": wl.max_len,
+                       "async_ratio": wl.alpha, "tokens_per_gpu": dw.T, "tokens_global": tokens_global,
+                       "chunk_tokens": chunk, "logits_pool_rows": dw.pool_rows,
+                       "l2": f"inputs larger than L2: logits pool {dw.pool_rows * wl.vocab * 2 / 1e9:.1f} GB, "
+                             f"dlogits chunk buffer {chunk * wl.vocab * 2 / 1e9:.1f} GB (L2 126 MB)",
+                       "accumulation": "fp32 softmax sums, fp64 per-token scalars and loss",
+                       "parallelism": f"dp{world} (whole GRPO groups LPT-sharded, one fp64 NCCL all-reduce)",
+                       "kernel": args.kernel},
+            "roofline": roof,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_2510_11345_b200 import synth as S
+
+    wl = S.WORKLOADS[args.workload]
+    variant = args.variant or wl.variant
+    if args.impl == "reference":
+        impl_reference(args, wl, variant)
+    else:
+        impl_ours(args, wl, variant)
+
+
+if __name__ == "__main__":
+    main()

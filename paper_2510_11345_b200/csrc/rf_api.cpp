@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -23,7 +24,7 @@ bool is_aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p
 
 struct RingGeometry {
     bool ok = false;
-    int cs = 1;
+    int cs = 1, ncw = 0, nvt = 0;
     int row_vecs = 0, slice_vecs = 0, nchunks = 0, nslots = 0;
     size_t smem = 0;
 };
@@ -40,10 +41,24 @@ int max_optin_smem() {
     return v;
 }
 
+int sm_smem_bytes() {
+    static int v = -1;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (v < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess) v = 0;
+    }
+    return v;
+}
+
 size_t dtype_size(int32_t d) { return d == RF_DTYPE_BF16 ? 2 : (d == RF_DTYPE_F32 ? 4 : 8); }
 
 // The ring kernel needs every logits row (and dlogits row) to start on a 16-byte
-// boundary with its 16-byte-padded length inside the row stride.
+// boundary with its 16-byte-padded length inside the row stride.  The row slice
+// of each CTA lives in registers: pick the smallest cluster whose slice fits
+// kRingThreads x NVT vectors, then the smallest NVT instance.
 RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
     RingGeometry g;
     const size_t es = dtype_size(b->logits_dtype), os = dtype_size(o->dlogits_dtype);
@@ -54,30 +69,47 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
     if (o->dlogits == nullptr || !is_aligned(o->dlogits, 16)) return g;
     if ((o->dlogits_row_stride * static_cast<int64_t>(os)) % 16 != 0) return g;
     if (o->dlogits_row_stride < static_cast<int64_t>(g.row_vecs) * epv) return g;
-    const int maxsmem = max_optin_smem();
-    const int nslots_max =
-        static_cast<int>((static_cast<size_t>(maxsmem) - rf::kRingTailBytes - 16) / (rf::kRingSlotBytes + 16));
+    const char* env = std::getenv("RF_RING_CONFIG");  // "small" (default) | "large" (experiments)
+    const bool large = env && std::strcmp(env, "large") == 0;
+    const int ncw = large ? rf::kRingWarpsLarge : rf::kRingWarpsSmall;
+    const int nct = ncw * 32;
+    // per-CTA shared memory: two CTAs per SM for the small configuration
+    int smem_cap = max_optin_smem();
+    if (!large) smem_cap = std::min(smem_cap, (sm_smem_bytes() - 2 * 1024) / 2);
     for (int cs = 1; cs <= 8; cs *= 2) {
         const int slice = (g.row_vecs + cs - 1) / cs;
         if (cs > 1 && slice * (cs - 1) >= g.row_vecs) break;  // every rank must own >= 1 vector
-        const int nchunks = (slice + rf::kRingChunkVecs - 1) / rf::kRingChunkVecs;
-        if (nchunks <= nslots_max - 1) {
-            g.cs = cs;
-            g.slice_vecs = slice;
-            g.nchunks = nchunks;
-            g.nslots = nslots_max;
-            g.smem = static_cast<size_t>(g.nslots) * (rf::kRingSlotBytes + 16) + 16 + rf::kRingTailBytes;
-            g.ok = true;
-            return g;
+        int nvt = 0;
+        if (large) {
+            nvt = (static_cast<int64_t>(27) * nct >= slice) ? 27 : 0;
+        } else {
+            for (int q : rf::kRingNvtSmall) {
+                if (static_cast<int64_t>(q) * nct >= slice) {
+                    nvt = q;
+                    break;
+                }
+            }
         }
+        if (!nvt) continue;
+        const size_t cb = rf::ring_chunk_bytes(ncw, nvt);
+        g.cs = cs;
+        g.ncw = ncw;
+        g.nvt = nvt;
+        g.slice_vecs = slice;
+        g.nchunks = static_cast<int>((slice + cb / 16 - 1) / (cb / 16));
+        // [nslots x (chunk + full/empty barriers)] + 4 row barriers + tail words
+        g.nslots = static_cast<int>((static_cast<size_t>(smem_cap) - rf::kRingTailBytes - 32) / (cb + 16));
+        g.smem = static_cast<size_t>(g.nslots) * (cb + 16) + 32 + rf::kRingTailBytes;
+        g.ok = g.nslots >= 2;
+        return g;
     }
     return g;
 }
 
-int ring_clusters(bool ib, bool ob, int cs, size_t smem) {
+int ring_clusters(bool ib, bool ob, int ncw, int nvt, int cs, size_t smem) {
     struct Key {
         bool ib, ob;
-        int cs;
+        int ncw, nvt, cs;
         size_t smem;
         int val;
     };
@@ -85,16 +117,16 @@ int ring_clusters(bool ib, bool ob, int cs, size_t smem) {
     static std::mutex mu;
     std::lock_guard<std::mutex> lk(mu);
     for (const Key& k : cache)
-        if (k.ib == ib && k.ob == ob && k.cs == cs && k.smem == smem) return k.val;
+        if (k.ib == ib && k.ob == ob && k.ncw == ncw && k.nvt == nvt && k.cs == cs && k.smem == smem) return k.val;
     int n = 0;
-    if (rf::ring_max_clusters(ib, ob, cs, smem, &n) != cudaSuccess || n <= 0) {
+    if (rf::ring_max_clusters(ib, ob, ncw, nvt, cs, smem, &n) != cudaSuccess || n <= 0) {
         cudaGetLastError();
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        n = sms / cs;
+        n = sms * rf::ring_min_blocks(ncw) / cs;
     }
-    cache.push_back({ib, ob, cs, smem, n});
+    cache.push_back({ib, ob, ncw, nvt, cs, smem, n});
     return n;
 }
 
@@ -347,9 +379,9 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.row_vecs = g.row_vecs;
             p.nchunks = g.nchunks;
             p.nslots = g.nslots;
-            const int maxc = ring_clusters(ib, ob, g.cs, g.smem);
+            const int maxc = ring_clusters(ib, ob, g.ncw, g.nvt, g.cs, g.smem);
             const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-            if (rf::launch_ring(p, ib, ob, g.cs, ncl, g.smem, s) != cudaSuccess) return RF_ERR_CUDA;
+            if (rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s) != cudaSuccess) return RF_ERR_CUDA;
             nparts = ncl;
         } else {
             const int grid = generic_grid(b->num_tokens);

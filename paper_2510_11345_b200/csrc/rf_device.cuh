@@ -288,41 +288,60 @@ __device__ __forceinline__ void variant_math(const KParams& p, double r, double 
     }
 }
 
-// token_mean per-token math given lp (losses.cpp:262-320).
-__device__ __forceinline__ TokenResult token_math(const KParams& p, int64_t t, double lp, double A,
-                                                  double token_scale) {
+__device__ __forceinline__ double token_scale_of(const KParams& p, int64_t seq) {
+    if (p.normalization == RF_NORM_GLOBAL_TOKEN) return p.inv_t;
+    const double len = static_cast<double>(p.seq_offsets[seq + 1] - p.seq_offsets[seq]);
+    return p.inv_n / len;
+}
+
+// The lp-independent half of the per-token math (loads + the theta-constant
+// factors), computed while the row's softmax is still being reduced.
+struct TokenPre {
+    double b, lq, A, scale, m, po;
+    uint32_t flags;
+};
+
+__device__ __forceinline__ TokenPre token_pre(const KParams& p, int64_t t, int64_t seq) {
+    TokenPre q;
+    q.flags = 0;
+    q.b = load_logp(p.behavior_logp, t, p.logp_f64);
+    q.A = p.advantages[seq];
+    q.scale = token_scale_of(p, seq);
+    q.m = 1.0;
+    if (p.mismatch_cap > 0.0) {  // losses.cpp:170-176
+        const double em = exp(q.b - load_logp(p.engine_logp, t, p.logp_f64));
+        q.m = (p.mismatch_cap < em) ? p.mismatch_cap : em;
+        if (em > p.mismatch_cap) q.flags |= RF_FLAG_MISMATCH_CAPPED;
+    }
+    q.lq = 0.0;
+    q.po = 0.0;
+    if (p.variant == RF_DECOUPLED_PPO) {  // losses.cpp:283-284
+        q.lq = load_logp(p.prox_logp, t, p.logp_f64);
+        q.po = exp(q.lq - q.b);
+    }
+    return q;
+}
+
+// The lp-dependent half (losses.cpp:264-320).
+__device__ __forceinline__ TokenResult token_post(const KParams& p, const TokenPre& q, double lp) {
     TokenResult o;
-    o.flags = 0;
-    const double b = load_logp(p.behavior_logp, t, p.logp_f64);
-    const double lr = lp - b;
-    const double r = exp(lr);
+    o.flags = q.flags;
+    const double r = exp(lp - q.b);
     o.ratio = r;
     if (!isfinite(r)) o.flags |= RF_FLAG_NONFINITE;
-    double m = 1.0;
-    if (p.mismatch_cap > 0.0) {
-        const double em = exp(b - load_logp(p.engine_logp, t, p.logp_f64));
-        m = (p.mismatch_cap < em) ? p.mismatch_cap : em;
-        if (em > p.mismatch_cap) o.flags |= RF_FLAG_MISMATCH_CAPPED;
-    }
-    double po = 0.0, tp = 0.0;
-    if (p.variant == RF_DECOUPLED_PPO) {
-        const double lq = load_logp(p.prox_logp, t, p.logp_f64);
-        po = exp(lq - b);
-        tp = exp(lp - lq);
-    }
+    const double tp = (p.variant == RF_DECOUPLED_PPO) ? exp(lp - q.lq) : 0.0;
     double value, gw;
-    variant_math(p, r, A, po, tp, lp, value, gw, o.flags);
-    const double sm = __dmul_rn(token_scale, m);
+    variant_math(p, r, q.A, q.po, tp, lp, value, gw, o.flags);
+    const double sm = __dmul_rn(q.scale, q.m);
     o.k = __dmul_rn(p.grad_sign, __dmul_rn(sm, gw));
     o.loss = __dmul_rn(sm, value);
     if (o.k == 0.0) o.flags |= RF_FLAG_ZERO_COEF;
     return o;
 }
 
-__device__ __forceinline__ double token_scale_of(const KParams& p, int64_t seq) {
-    if (p.normalization == RF_NORM_GLOBAL_TOKEN) return p.inv_t;
-    const double len = static_cast<double>(p.seq_offsets[seq + 1] - p.seq_offsets[seq]);
-    return p.inv_n / len;
+// token_mean per-token math given lp (losses.cpp:262-320).
+__device__ __forceinline__ TokenResult token_math(const KParams& p, int64_t t, double lp, int64_t seq) {
+    return token_post(p, token_pre(p, t, seq), lp);
 }
 
 // Partial-scalar accumulator kept by the thread that owns a partial slot.

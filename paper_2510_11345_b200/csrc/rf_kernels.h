@@ -1,4 +1,4 @@
-// rf_kernels.h — launch entry points of rf_kernels.cu (internal to the library).
+// rf_kernels.h — launch entry points of the kernels (internal to the library).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -6,17 +6,24 @@
 
 namespace rf {
 
-constexpr int kRingWarps = 8;   // consumer warps per CTA (+1 producer warp)
-constexpr int kRingVPT = 4;     // 16-byte vectors per consumer thread per chunk
-constexpr int kRingChunkVecs = kRingWarps * 32 * kRingVPT;
-constexpr size_t kRingSlotBytes = static_cast<size_t>(kRingChunkVecs) * 16 + kRingWarps * 32 * 4;
-constexpr size_t kRingTailBytes = 512;  // barriers' tail: exchange/reduce/broadcast words
+// Ring kernel (rf_ring.cu) configurations.  A CTA = NCW consumer warps + 1
+// producer warp; the CTA's row slice lives in registers (NVT 16-byte vectors
+// per consumer thread).
+//   small: 5 + 1 warps, two CTAs per SM (168 registers), NVT in {4, 16, 30}
+//   large: 11 + 1 warps, one CTA per SM (168 registers), NVT = 27
+constexpr int kRingWarpsSmall = 5;
+constexpr int kRingWarpsLarge = 11;
+constexpr int kRingNvtSmall[3] = {4, 16, 30};
+__host__ __device__ constexpr int ring_min_blocks(int ncw) { return ncw <= kRingWarpsSmall ? 2 : 1; }
+__host__ __device__ constexpr int ring_vpc(int nvt) { return nvt >= 9 ? 3 : 2; }  // vectors/thread/TMA chunk
+constexpr size_t ring_chunk_bytes(int ncw, int nvt) { return static_cast<size_t>(ncw) * 32 * ring_vpc(nvt) * 16; }
+constexpr size_t kRingTailBytes = 512;  // exchange / reduce / broadcast words
 constexpr int kGenericThreads = 256;
 constexpr int kGenericMaxGrid = 148 * 8;
 
-cudaError_t launch_ring(const KParams& p, bool in_bf16, bool out_bf16, int cs, int nclusters, size_t smem,
-                        cudaStream_t st);
-cudaError_t ring_max_clusters(bool in_bf16, bool out_bf16, int cs, size_t smem, int* out);
+cudaError_t launch_ring(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
+                        size_t smem, cudaStream_t st);
+cudaError_t ring_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);
 cudaError_t launch_generic(const KParams& p, bool in_bf16, bool out_bf16, int grid, cudaStream_t st);
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st);
 cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, cudaStream_t st);
