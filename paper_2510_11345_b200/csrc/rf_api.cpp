@@ -24,6 +24,7 @@ bool is_aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p
 
 struct RingGeometry {
     bool ok = false;
+    int kind = 2;  // 0 small, 1 large, 2 lag
     int cs = 1, ncw = 0, nvt = 0;
     int row_vecs = 0, slice_vecs = 0, nchunks = 0, nslots = 0;
     size_t smem = 0;
@@ -69,21 +70,25 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
     if (o->dlogits == nullptr || !is_aligned(o->dlogits, 16)) return g;
     if ((o->dlogits_row_stride * static_cast<int64_t>(os)) % 16 != 0) return g;
     if (o->dlogits_row_stride < static_cast<int64_t>(g.row_vecs) * epv) return g;
-    const char* env = std::getenv("RF_RING_CONFIG");  // "small" (default) | "large" (experiments)
-    const bool large = env && std::strcmp(env, "large") == 0;
-    const int ncw = large ? rf::kRingWarpsLarge : rf::kRingWarpsSmall;
+    // RF_RING_CONFIG: "lag" (default: TMEM-parked previous row, 1 CTA/SM),
+    // "small" (2 CTAs/SM, register-resident) or "large" (1 CTA/SM, register-resident).
+    const char* env = std::getenv("RF_RING_CONFIG");
+    g.kind = 2;
+    if (env && std::strcmp(env, "small") == 0) g.kind = 0;
+    if (env && std::strcmp(env, "large") == 0) g.kind = 1;
+    const int ncw = g.kind == 2 ? rf::kRingWarpsLag : (g.kind == 1 ? rf::kRingWarpsLarge : rf::kRingWarpsSmall);
     const int nct = ncw * 32;
-    // per-CTA shared memory: two CTAs per SM for the small configuration
     int smem_cap = max_optin_smem();
-    if (!large) smem_cap = std::min(smem_cap, (sm_smem_bytes() - 2 * 1024) / 2);
+    if (g.kind == 0) smem_cap = std::min(smem_cap, (sm_smem_bytes() - 2 * 1024) / 2);  // two CTAs per SM
+    const size_t tail = g.kind == 2 ? rf::kRingLagTailBytes + rf::kRingLagBarrierBytes : rf::kRingTailBytes + 32;
     for (int cs = 1; cs <= 8; cs *= 2) {
         const int slice = (g.row_vecs + cs - 1) / cs;
         if (cs > 1 && slice * (cs - 1) >= g.row_vecs) break;  // every rank must own >= 1 vector
         int nvt = 0;
-        if (large) {
+        if (g.kind == 1) {
             nvt = (static_cast<int64_t>(27) * nct >= slice) ? 27 : 0;
         } else {
-            for (int q : rf::kRingNvtSmall) {
+            for (int q : (g.kind == 2 ? rf::kRingNvtLag : rf::kRingNvtSmall)) {
                 if (static_cast<int64_t>(q) * nct >= slice) {
                     nvt = q;
                     break;
@@ -97,19 +102,19 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
         g.nvt = nvt;
         g.slice_vecs = slice;
         g.nchunks = static_cast<int>((slice + cb / 16 - 1) / (cb / 16));
-        // [nslots x (chunk + full/empty barriers)] + 4 row barriers + tail words
-        g.nslots = static_cast<int>((static_cast<size_t>(smem_cap) - rf::kRingTailBytes - 32) / (cb + 16));
-        g.smem = static_cast<size_t>(g.nslots) * (cb + 16) + 32 + rf::kRingTailBytes;
+        // [nslots x (chunk + full/empty barriers)] + row barriers + tail words
+        g.nslots = static_cast<int>((static_cast<size_t>(smem_cap) - tail) / (cb + 16));
+        g.smem = static_cast<size_t>(g.nslots) * (cb + 16) + tail;
         g.ok = g.nslots >= 2;
         return g;
     }
     return g;
 }
 
-int ring_clusters(bool ib, bool ob, int ncw, int nvt, int cs, size_t smem) {
+int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t smem) {
     struct Key {
         bool ib, ob;
-        int ncw, nvt, cs;
+        int kind, ncw, nvt, cs;
         size_t smem;
         int val;
     };
@@ -117,16 +122,20 @@ int ring_clusters(bool ib, bool ob, int ncw, int nvt, int cs, size_t smem) {
     static std::mutex mu;
     std::lock_guard<std::mutex> lk(mu);
     for (const Key& k : cache)
-        if (k.ib == ib && k.ob == ob && k.ncw == ncw && k.nvt == nvt && k.cs == cs && k.smem == smem) return k.val;
+        if (k.ib == ib && k.ob == ob && k.kind == kind && k.ncw == ncw && k.nvt == nvt && k.cs == cs &&
+            k.smem == smem)
+            return k.val;
     int n = 0;
-    if (rf::ring_max_clusters(ib, ob, ncw, nvt, cs, smem, &n) != cudaSuccess || n <= 0) {
+    const cudaError_t e = kind == 2 ? rf::ring_lag_max_clusters(ib, ob, nvt, cs, smem, &n)
+                                    : rf::ring_max_clusters(ib, ob, ncw, nvt, cs, smem, &n);
+    if (e != cudaSuccess || n <= 0) {
         cudaGetLastError();
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        n = sms * rf::ring_min_blocks(ncw) / cs;
+        n = sms * (kind == 0 ? 2 : 1) / cs;
     }
-    cache.push_back({ib, ob, ncw, nvt, cs, smem, n});
+    cache.push_back({ib, ob, kind, ncw, nvt, cs, smem, n});
     return n;
 }
 
@@ -379,9 +388,11 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.row_vecs = g.row_vecs;
             p.nchunks = g.nchunks;
             p.nslots = g.nslots;
-            const int maxc = ring_clusters(ib, ob, g.ncw, g.nvt, g.cs, g.smem);
+            const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
             const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-            if (rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s) != cudaSuccess) return RF_ERR_CUDA;
+            const cudaError_t e = g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.nvt, g.cs, ncl, g.smem, s)
+                                              : rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
+            if (e != cudaSuccess) return RF_ERR_CUDA;
             nparts = ncl;
         } else {
             const int grid = generic_grid(b->num_tokens);

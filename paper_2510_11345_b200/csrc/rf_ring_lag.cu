@@ -1,0 +1,490 @@
+// rf_ring_lag.cu — K2 "lag" variant: the fused off-policy loss + dlogits kernel
+// with the per-row softmax/coefficient round trip taken off the critical path.
+//
+// Same data path as rf_ring.cu (one HBM read of every logits row, one HBM write of
+// its dlogits row; TMA bulk loads into a shared-memory ring; the row slice held
+// in the register file during the exp sweep), but the consumer warps never wait
+// for the row coefficient of the row they just reduced:
+//
+//   row i   : copy-in + max + exp sweep in registers -> partial (M,S) -> scalar warp
+//             e_i parked in TENSOR MEMORY (tcgen05.st, 120 columns per thread)
+//   row i+1 : copy-in + max + exp sweep in registers -> partial -> scalar warp
+//   row i   : wait k_i (computed by the scalar warp while row i+1 streamed in),
+//             read e_i back from TMEM (tcgen05.ld) and write its dlogits
+//
+// TMEM (256 KB per SM, unused by this non-GEMM path) is the second row buffer
+// next to the register file; the scalar warp (DSMEM cluster exchange + fp64
+// surrogate math, losses.cpp:264-320) has a whole row of streaming to finish.
+// One CTA per SM (12 warps: 10 consumers, 1 TMA producer, 1 scalar), 2-CTA
+// clusters for the Qwen3 vocabulary.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "rf_device.cuh"
+#include "rf_kernels.h"
+#include "rf_ring_common.cuh"
+
+namespace rf {
+
+using namespace ring;
+
+namespace {
+
+__device__ __forceinline__ void tmem_alloc(uint32_t smem_dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint4& v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// Two 4-column loads and the wait that makes them usable; the loaded registers are
+// threaded through the wait so no consumer can be scheduled above it.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint4& a, uint4& b) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%8];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%9];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "r"(taddr), "r"(taddr + 4)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint4& a) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+        : "r"(taddr)
+        : "memory");
+}
+
+}  // namespace
+
+template <bool IN_BF16, bool OUT_BF16, int NCW, int NVT>
+__global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __grid_constant__ KParams p) {
+    constexpr int NCT = NCW * 32;
+    constexpr int EPV = IN_BF16 ? 8 : 4;
+    constexpr int VPC = ring_vpc(NVT);
+    constexpr int NCH = (NVT + VPC - 1) / VPC;
+    constexpr int CHUNK_VECS = NCT * VPC;
+    constexpr uint32_t CHUNK_BYTES = CHUNK_VECS * 16;
+    constexpr size_t OES = OUT_BF16 ? 2 : 4;
+    constexpr size_t IES = IN_BF16 ? 2 : 4;
+    static_assert(NVT * 4 <= 256, "a thread's e values must fit its 256 TMEM columns");
+    static_assert(NCW == 8, "two consumer warpgroups (TMEM lane quarters x 2 column halves)");
+
+    // smem: [nslots chunks][full][empty][x(2)][red(2)][bc(2)] + tail
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int nslots = p.nslots;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar_full = sbase + nslots * CHUNK_BYTES;
+    const uint32_t bar_empty = bar_full + nslots * 8;
+    const uint32_t bar_x = bar_empty + nslots * 8;  // [2] cluster exchange (row parity)
+    const uint32_t bar_red = bar_x + 16;             // [2] consumers -> scalar: CTA partial (row parity)
+    const uint32_t bar_bc = bar_red + 16;            // [2] scalar -> consumers: coefficient (row parity)
+    uint8_t* tail = smem + nslots * CHUNK_BYTES + nslots * 16 + 48;
+    double* xS = reinterpret_cast<double*>(tail);              // [2][8]
+    float* xM = reinterpret_cast<float*>(tail + 128);          // [2][8]
+    double* redS = reinterpret_cast<double*>(tail + 192);      // [2][NCW]
+    float* redM = reinterpret_cast<float*>(tail + 192 + 16 * NCW);  // [2][NCW]
+    struct Bcast {
+        double ctaS;
+        float ctaM, lseL;
+        double k, tok_val;
+        float negk;
+        int32_t tok;
+    };
+    Bcast* bcs = reinterpret_cast<Bcast*>(tail + 192 + 24 * NCW + ((24 * NCW) % 8 ? 4 : 0));  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bcs + 2);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_ctarank();
+    const uint32_t csize = cluster_nctarank();
+    const uint32_t cid = cluster_id_x();
+    const uint32_t ncl = ncluster_x();
+
+    if (tid == 0) {
+        for (int s = 0; s < nslots; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, NCW);
+        }
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(bar_x + 8 * q, csize > 1 ? csize - 1 : 1);
+            mbar_init(bar_red + 8 * q, 1);
+            mbar_init(bar_bc + 8 * q, 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_fence_before();
+    cluster_sync_all();
+    tmem_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int slice_begin = static_cast<int>(rank) * p.slice_vecs;
+    const int slice_len = max(0, min(p.slice_vecs, p.row_vecs - slice_begin));
+    const int nchunks = (slice_len + CHUNK_VECS - 1) / CHUNK_VECS;
+    const int tail_vec = p.row_vecs - 1;
+    const int tail_valid = p.V - tail_vec * EPV;  // 1..EPV
+    const bool has_tail = tail_valid < EPV;
+
+    // Warpgroup 2 (producer, scalar, 2 idle warps) hands registers to the two
+    // consumer warpgroups, whose row slices live in the register file.
+    // Each register-budget region runs to its own epilogue (ptxas allocates
+    // registers per region after setmaxnreg).
+    if (warp >= NCW) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kLagRegsSupport));
+        if (warp == NCW) {
+        // ------------------------------ TMA producer ------------------------------
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int s = 0;
+            uint32_t phase = 0, uses = 0;
+            for (int64_t t = cid; t < p.T; t += ncl) {
+                const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(p.logits) + (row * p.row_stride) * IES +
+                                     static_cast<size_t>(slice_begin) * 16;
+                for (int c = 0; c < nchunks; ++c) {
+                    if (uses >= static_cast<uint32_t>(nslots)) mbar_wait(bar_empty + 8 * s, phase);
+                    const int nv = min(CHUNK_VECS, slice_len - c * CHUNK_VECS);
+                    const uint32_t bytes = static_cast<uint32_t>(nv) * 16;
+                    mbar_arrive_expect_tx(bar_full + 8 * s, bytes);
+                    bulk_g2s(sbase + s * CHUNK_BYTES, src + static_cast<size_t>(c) * CHUNK_BYTES, bytes,
+                             bar_full + 8 * s, pol);
+                    ++uses;
+                    if (++s == nslots) {
+                        s = 0;
+                        if (uses > static_cast<uint32_t>(nslots)) phase ^= 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == NCW + 1) {
+        // --------------------------------- scalar ---------------------------------
+        if (lane == 0) {
+            Partials part;
+            part.zero();
+            uint32_t row_iter = 0;
+            for (int64_t t = cid; t < p.T; t += ncl, ++row_iter) {
+                const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
+                const int32_t tok = p.token_ids[t];
+                const bool tok_ok = tok >= 0 && tok < p.V;
+                const float x_tok = tok_ok ? load_logit(p.logits, row * p.row_stride + tok, IN_BF16) : 0.0f;
+                const TokenPre pre = token_pre(p, t, p.seq_of_token[t]);
+                const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
+                Bcast* bc = bcs + par;
+                mbar_wait(bar_red + 8 * par, ph);
+                const float Mw = bc->ctaM;
+                const double Sw = bc->ctaS;
+                double Mc = static_cast<double>(Mw), Sc = Sw;
+                if (csize > 1) {
+                    const uint32_t myS = smem_u32(&xS[par * 8 + rank]);
+                    const uint32_t myM = smem_u32(&xM[par * 8 + rank]);
+                    for (uint32_t q = 0; q < csize; ++q) {
+                        if (q == rank) continue;
+                        st_cluster_f64(mapa(myS, q), Sw);
+                        st_cluster_f32(mapa(myM, q), Mw);
+                    }
+                    for (uint32_t q = 0; q < csize; ++q) {
+                        if (q == rank) continue;
+                        mbar_arrive_remote(mapa(bar_x + 8 * par, q));
+                    }
+                    mbar_wait_cluster(bar_x + 8 * par, ph);
+                    float Mx = -CUDART_INF_F;
+                    for (uint32_t q = 0; q < csize; ++q) Mx = fmaxf(Mx, (q == rank) ? Mw : xM[par * 8 + q]);
+                    Sc = 0.0;
+                    for (uint32_t q = 0; q < csize; ++q) {  // rank order: identical on every CTA
+                        const float Mq = (q == rank) ? Mw : xM[par * 8 + q];
+                        const double Sq = (q == rank) ? Sw : xS[par * 8 + q];
+                        if (Sq != 0.0) Sc += Sq * exp2(static_cast<double>(Mq) - static_cast<double>(Mx));
+                    }
+                    Mc = static_cast<double>(Mx);
+                }
+                const double lse = 0.69314718055994530942 * (Mc + log2(Sc));  // natural-log lse
+                TokenResult tr;
+                double lp = CUDART_NAN;
+                if (!tok_ok) {
+                    atomicOr(p.status, RF_DEVSTAT_TOKEN_OUT_OF_RANGE);
+                    tr.ratio = CUDART_NAN;
+                    tr.k = 0.0;
+                    tr.loss = 0.0;
+                    tr.flags = RF_FLAG_NONFINITE | RF_FLAG_ZERO_COEF;
+                } else {
+                    lp = static_cast<double>(x_tok) - lse;
+                    tr = token_post(p, pre, lp);
+                    if (tr.flags & RF_FLAG_NONFINITE) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
+                }
+                bc->k = tr.k;
+                bc->tok_val = (tok_ok && tr.k != 0.0) ? tr.k - tr.k * exp(lp) : 0.0;
+                bc->lseL = static_cast<float>(lse * 1.4426950408889634);
+                bc->negk = static_cast<float>(-tr.k);
+                bc->tok = tok_ok ? tok : -1;
+                mbar_arrive(bar_bc + 8 * par);
+                if (rank == 0) {
+                    if (p.token_logp) p.token_logp[t] = lp;
+                    if (p.token_ratio) p.token_ratio[t] = tr.ratio;
+                    if (p.token_coef) p.token_coef[t] = tr.k;
+                    if (p.token_loss) p.token_loss[t] = tr.loss;
+                    if (p.token_flags) p.token_flags[t] = static_cast<uint8_t>(tr.flags);
+                    part.add_token(tr, 0.0);
+                }
+            }
+            if (rank == 0) part.store(p.partials + static_cast<size_t>(cid) * RF_NUM_SCALARS);
+        }
+        __syncwarp();
+        }
+        tmem_fence_before();
+        __syncwarp();
+        cluster_sync_all();
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kLagRegsConsumer));
+    {
+        // -------------------------------- consumers --------------------------------
+        int s = 0;
+        uint32_t fphase = 0;
+        const uint64_t L2 = pk2(1.4426950408889634f, 1.4426950408889634f);
+        const uint32_t tm = tmem_base + ((32u * (warp & 3)) << 16) + 256u * (warp >> 2);
+        uint4 r[NVT];
+        // Thread-constant geometry: vector j of this thread is slice vector
+        // sv(j) = (j/VPC)·CHUNK_VECS + (j%VPC)·NCT + tid, increasing in j, so the valid
+        // ones are j < jmax; tail_j is the j holding the row's padded tail vector.
+        int jmax = 0;
+#pragma unroll
+        for (int j = 0; j < NVT; ++j) jmax += ((j / VPC) * CHUNK_VECS + (j % VPC) * NCT + tid < slice_len) ? 1 : 0;
+        int tail_j = -1;
+        if (has_tail) {
+            const int svt = tail_vec - slice_begin;
+            if (svt >= 0 && svt < slice_len && (svt % CHUNK_VECS) % NCT == tid)
+                tail_j = (svt / CHUNK_VECS) * VPC + (svt % CHUNK_VECS) / NCT;
+        }
+        const size_t thr_off = static_cast<size_t>(slice_begin + tid) * EPV * OES;
+
+        // copy-in + max + exp sweep + CTA reduction of row t into r[]; returns C_t.
+        auto stream_row = [&](uint32_t row_iter) -> float {
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                if (c < nchunks) {
+                    mbar_wait(bar_full + 8 * s, fphase);
+                    const uint32_t slot = sbase + s * CHUNK_BYTES;
+#pragma unroll
+                    for (int jj = 0; jj < VPC; ++jj) {
+                        const int j = c * VPC + jj;
+                        if (j < NVT)
+                            r[j] = (j < jmax) ? lds128(slot + (jj * NCT + tid) * 16) : neg_inf_vec<IN_BF16>();
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_empty + 8 * s);
+                    if (++s == nslots) {
+                        s = 0;
+                        fphase ^= 1;
+                    }
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < VPC; ++jj) {
+                        const int j = c * VPC + jj;
+                        if (j < NVT) r[j] = neg_inf_vec<IN_BF16>();
+                    }
+                }
+            }
+            if (tail_j >= 0) {
+#pragma unroll
+                for (int j = 0; j < NVT; ++j)
+                    if (j == tail_j) mask_tail<IN_BF16>(r[j], tail_valid);
+            }
+            float M;
+            if (IN_BF16) {
+                uint32_t m2 = vec_max2<true>(r[0]);
+#pragma unroll
+                for (int j = 1; j < NVT; ++j) {
+                    const uint32_t v2 = vec_max2<true>(r[j]);
+                    __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&m2);
+                    __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&v2);
+                    a = __hmax2(a, b);
+                    m2 = *reinterpret_cast<uint32_t*>(&a);
+                }
+                M = fmaxf(bf16lo(m2), bf16hi(m2));
+            } else {
+                M = __uint_as_float(vec_max2<false>(r[0]));
+#pragma unroll
+                for (int j = 1; j < NVT; ++j) M = fmaxf(M, __uint_as_float(vec_max2<false>(r[j])));
+            }
+            const float Mt = (M == -CUDART_INF_F) ? 0.0f : M;
+            const float C = Mt * 1.4426950408889634f;
+            const uint64_t negC2 = pk2(-C, -C);
+            double S = 0.0;
+#pragma unroll
+            for (int j = 0; j < NVT; ++j) {
+                const uint64_t acc = vec_exp<IN_BF16>(r[j], L2, negC2);
+                S += static_cast<double>(lo2(acc) + hi2(acc));
+            }
+            const float Mr = (S == 0.0) ? -CUDART_INF_F : C;
+            // CTA reduction of (C, S) pairs in the log2 domain -> scalar warp
+            const uint32_t par = row_iter & 1;
+            float Mw = Mr;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
+            double sw = (S != 0.0) ? S * exp2(static_cast<double>(Mr) - static_cast<double>(Mw)) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sw += __shfl_xor_sync(0xffffffffu, sw, o);
+            if (lane == 0) {
+                redM[par * NCW + warp] = Mw;
+                redS[par * NCW + warp] = sw;
+            }
+            named_bar_sync(1, NCT);
+            if (warp == 0) {
+                const float Mq = lane < NCW ? redM[par * NCW + lane] : -CUDART_INF_F;
+                const double Sq = lane < NCW ? redS[par * NCW + lane] : 0.0;
+                float Mx = Mq;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+                double sx = (Sq != 0.0) ? Sq * exp2(static_cast<double>(Mq) - static_cast<double>(Mx)) : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+                if (lane == 0) {
+                    bcs[par].ctaM = Mx;
+                    bcs[par].ctaS = sx;
+                    mbar_arrive(bar_red + 8 * par);
+                }
+            }
+            return C;
+        };
+
+        // write the dlogits row t (coefficient of row_iter) from registers or TMEM
+        auto write_row = [&](int64_t t, uint32_t row_iter, float C) {
+            const uint32_t par = row_iter & 1;
+            mbar_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
+            const Bcast* bc = bcs + par;
+            const float lseL = bc->lseL;
+            const float negk = bc->negk;
+            const bool zero = (bc->k == 0.0);
+            const int tokv = bc->tok;
+            const float tv = static_cast<float>(bc->tok_val);
+            const float f = zero ? 0.0f : negk * ex2_approx(C - lseL);
+            const uint64_t f2 = pk2(f, f);
+            uint8_t* drow = reinterpret_cast<uint8_t*>(p.dlogits) + static_cast<size_t>(t) * p.dl_stride * OES;
+            uint8_t* dthr = drow + thr_off;
+#pragma unroll
+            for (int j = 0; j < NVT; j += 2) {
+                uint4 e0, e1;
+                if (j + 1 < NVT)
+                    tmem_ld8(tm + 4 * j, e0, e1);
+                else
+                    tmem_ld4(tm + 4 * j, e0);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int jj = j + h;
+                    if (jj >= NVT) break;
+                    const uint4& e = h ? e1 : e0;
+                    if (jj < jmax) {
+                        uint8_t* dst = dthr + static_cast<size_t>((jj / VPC) * CHUNK_VECS + (jj % VPC) * NCT) * EPV * OES;
+                        if (jj != tail_j)
+                            store_vec<OUT_BF16, EPV>(dst, e, f2, IN_BF16);
+                        else
+                            store_vec_partial<OUT_BF16, EPV>(dst, e, f, IN_BF16, tail_valid);
+                    }
+                }
+            }
+            if (tokv >= 0) {  // sampled-token fix-up by the thread that stored its vector
+                const int sv = tokv / EPV - slice_begin;
+                if (sv >= 0 && sv < slice_len && (sv % CHUNK_VECS) % NCT == tid) {
+                    if (OUT_BF16)
+                        reinterpret_cast<__nv_bfloat16*>(drow)[tokv] = __float2bfloat16_rn(tv);
+                    else
+                        reinterpret_cast<float*>(drow)[tokv] = tv;
+                }
+            }
+        };
+
+        uint32_t it = 0;
+        int64_t t = cid;
+        float C = 0.f;
+        if (t < p.T) C = stream_row(0);
+        while (t < p.T) {
+            // park e_t in TMEM, stream row t + ncl (if any), then write row t from TMEM
+#pragma unroll
+            for (int j = 0; j < NVT; ++j) tmem_st4(tm + 4 * j, r[j]);
+            tmem_wait_st();
+            const int64_t tn = t + ncl;
+            float Cn = 0.f;
+            if (tn < p.T) Cn = stream_row(it + 1);
+            write_row(t, it, C);
+            C = Cn;
+            t = tn;
+            ++it;
+        }
+    }
+    tmem_fence_before();
+    __syncwarp();
+    cluster_sync_all();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(tmem_base, 512);
+}
+
+namespace {
+
+template <bool IB, bool OB, int NVT>
+cudaError_t launch_lag_t(const KParams& p, int cs, int nclusters, size_t smem, cudaStream_t st, int* maxc) {
+    auto kern = ring_lag_kernel<IB, OB, kRingWarpsLag, NVT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((maxc ? 148 : nclusters) * cs));
+    cfg.blockDim = dim3((kRingWarpsLag + 4) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(cs);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (maxc) return cudaOccupancyMaxActiveClusters(maxc, kern, &cfg);
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <bool IB, bool OB>
+cudaError_t lag_nvt(const KParams& p, int nvt, int cs, int ncl, size_t smem, cudaStream_t st, int* maxc) {
+    switch (nvt) {
+        case 4: return launch_lag_t<IB, OB, 4>(p, cs, ncl, smem, st, maxc);
+        case 16: return launch_lag_t<IB, OB, 16>(p, cs, ncl, smem, st, maxc);
+        case 38: return launch_lag_t<IB, OB, 38>(p, cs, ncl, smem, st, maxc);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t lag_dispatch(const KParams& p, bool ib, bool ob, int nvt, int cs, int ncl, size_t smem, cudaStream_t st,
+                         int* maxc) {
+    if (ib && ob) return lag_nvt<true, true>(p, nvt, cs, ncl, smem, st, maxc);
+    if (ib && !ob) return lag_nvt<true, false>(p, nvt, cs, ncl, smem, st, maxc);
+    if (!ib && ob) return lag_nvt<false, true>(p, nvt, cs, ncl, smem, st, maxc);
+    return lag_nvt<false, false>(p, nvt, cs, ncl, smem, st, maxc);
+}
+
+}  // namespace
+
+cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int nvt, int cs, int nclusters,
+                            size_t smem, cudaStream_t st) {
+    return lag_dispatch(p, in_bf16, out_bf16, nvt, cs, nclusters, smem, st, nullptr);
+}
+
+cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int nvt, int cs, size_t smem, int* out) {
+    KParams p{};
+    return lag_dispatch(p, in_bf16, out_bf16, nvt, cs, 0, smem, nullptr, out);
+}
+
+}  // namespace rf
