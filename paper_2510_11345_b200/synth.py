@@ -187,16 +187,7 @@ def staleness(seed: int, n: int, alpha: int) -> np.ndarray:
     return np.array([rng.below(alpha + 1) for _ in range(n)], dtype=np.int64)
 
 
-def lpt_shard(group_tokens: np.ndarray, world: int) -> List[List[int]]:
-    """Longest-processing-time assignment of whole GRPO groups to ranks."""
-    order = np.argsort(-group_tokens, kind="stable")
-    load = np.zeros(world, dtype=np.int64)
-    out: List[List[int]] = [[] for _ in range(world)]
-    for g in order:
-        r = int(np.argmin(load))
-        out[r].append(int(g))
-        load[r] += int(group_tokens[g])
-    return [sorted(x) for x in out]
+from .dist import lpt_shard  # noqa: E402  (whole-group LPT sharding)
 
 
 @dataclass

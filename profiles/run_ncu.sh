@@ -6,5 +6,5 @@ CMD="python bench.py --steps 1 --warmup 1 --prompts 32 --no-e2e --no-cpu-baselin
 mkdir -p gpurun_out
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:ring_kernel -s 2 -c 1 -o gpurun_out/${TAG}_ring $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:ring -s 2 -c 1 -o gpurun_out/${TAG}_ring $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo done
