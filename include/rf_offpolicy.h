@@ -218,6 +218,11 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* cfg, const rf_batch* batch, 
  * thread (for benchmark accounting). */
 int32_t rf_last_launch_count(void);
 
+/* Profiling aid: per-phase cycle counters of the fused kernel, accumulated when
+ * the process runs with RF_DEBUG_COUNTERS=1 (else returns 0).  Synchronises the
+ * device; copies up to n counters into out and optionally resets them. */
+int32_t rf_debug_counters(uint64_t* out, int32_t n, int32_t reset);
+
 /* ---- host API: the reference-facing call with HOST buffers ----
  * Same semantics as rf_loss_and_grad but every pointer in batch/outputs is a
  * host pointer (pinned memory recommended).  Streams the batch through the GPU

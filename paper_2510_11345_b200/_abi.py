@@ -11,7 +11,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librf_offpolicy.so")
+# RF_LIB_VARIANT=phase loads the profiling build (per-phase cycle counters compiled in).
+LIB_PATH = os.path.join(_HERE, "librf_offpolicy_phase.so" if os.environ.get("RF_LIB_VARIANT") == "phase"
+                        else "librf_offpolicy.so")
 
 # enums (rf_offpolicy.h)
 RF_PPO, RF_DECOUPLED_PPO, RF_TIS, RF_CISPO, RF_TOPR, RF_GRPO, RF_NAIVE_IS = range(7)
@@ -137,6 +139,7 @@ EXPORTED_SYMBOLS = (
     "rf_loss_and_grad_ex",
     "rf_last_launch_count",
     "rf_loss_and_grad_host",
+    "rf_debug_counters",
 )
 
 _lib = None
@@ -178,5 +181,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rf_last_launch_count.restype = _i32
     lib.rf_loss_and_grad_host.argtypes = [P(rf_loss_config), P(rf_batch), P(rf_outputs), _i32, _i64]
     lib.rf_loss_and_grad_host.restype = _i32
+    lib.rf_debug_counters.argtypes = [_p, _i32, _i32]
+    lib.rf_debug_counters.restype = _i32
     _lib = lib
     return lib

@@ -76,7 +76,10 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
     g.kind = 2;
     if (env && std::strcmp(env, "small") == 0) g.kind = 0;
     if (env && std::strcmp(env, "large") == 0) g.kind = 1;
-    const int ncw = g.kind == 2 ? rf::kRingWarpsLag : (g.kind == 1 ? rf::kRingWarpsLarge : rf::kRingWarpsSmall);
+    int lag_ncw = rf::kRingWarpsLag;  // RF_LAG_WARPS=8|12|16 (experiments; 8 and 16 are bf16->bf16 only)
+    if (const char* lw = std::getenv("RF_LAG_WARPS")) lag_ncw = std::atoi(lw);
+    if (lag_ncw != 8 && lag_ncw != 12 && lag_ncw != 16) lag_ncw = rf::kRingWarpsLag;
+    const int ncw = g.kind == 2 ? lag_ncw : (g.kind == 1 ? rf::kRingWarpsLarge : rf::kRingWarpsSmall);
     const int nct = ncw * 32;
     int smem_cap = max_optin_smem();
     if (g.kind == 0) smem_cap = std::min(smem_cap, (sm_smem_bytes() - 2 * 1024) / 2);  // two CTAs per SM
@@ -87,6 +90,10 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
         int nvt = 0;
         if (g.kind == 1) {
             nvt = (static_cast<int64_t>(27) * nct >= slice) ? 27 : 0;
+        } else if (g.kind == 2 && ncw != rf::kRingWarpsLag) {
+            const int q = ncw == 8 ? rf::kRingNvtLag8 : rf::kRingNvtLag16;
+            const bool bf = b->logits_dtype == RF_DTYPE_BF16 && o->dlogits_dtype == RF_DTYPE_BF16;
+            nvt = (bf && static_cast<int64_t>(q) * nct >= slice) ? q : 0;
         } else {
             for (int q : (g.kind == 2 ? rf::kRingNvtLag : rf::kRingNvtSmall)) {
                 if (static_cast<int64_t>(q) * nct >= slice) {
@@ -126,7 +133,7 @@ int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t s
             k.smem == smem)
             return k.val;
     int n = 0;
-    const cudaError_t e = kind == 2 ? rf::ring_lag_max_clusters(ib, ob, nvt, cs, smem, &n)
+    const cudaError_t e = kind == 2 ? rf::ring_lag_max_clusters(ib, ob, ncw, nvt, cs, smem, &n)
                                     : rf::ring_max_clusters(ib, ob, ncw, nvt, cs, smem, &n);
     if (e != cudaSuccess || n <= 0) {
         cudaGetLastError();
@@ -172,6 +179,24 @@ WsLayout ws_layout(const rf_loss_config* c, const rf_batch* b, void* base) {
 }
 
 rf_status check_cuda(cudaError_t e) { return e == cudaSuccess ? RF_OK : RF_ERR_CUDA; }
+
+// Per-phase cycle counters of the lag kernel (profiling aid): enabled by the
+// environment variable RF_DEBUG_COUNTERS=1, read with rf_debug_counters().
+unsigned long long* debug_counters() {
+    static unsigned long long* buf = nullptr;
+    static int enabled = -1;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (enabled < 0) {
+        const char* e = std::getenv("RF_DEBUG_COUNTERS");
+        enabled = (e && e[0] == '1') ? 1 : 0;
+        if (enabled && cudaMalloc(&buf, 16 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(buf, 0, 16 * sizeof(unsigned long long));
+        else
+            buf = nullptr;
+    }
+    return buf;
+}
 
 }  // namespace
 
@@ -259,6 +284,16 @@ size_t rf_workspace_bytes(const rf_loss_config* c, const rf_batch* b) {
 }
 
 int32_t rf_last_launch_count(void) { return g_last_launches; }
+
+int32_t rf_debug_counters(uint64_t* out, int32_t n, int32_t reset) {
+    unsigned long long* buf = debug_counters();
+    if (!buf || !out || n <= 0) return 0;
+    n = n > 16 ? 16 : n;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, buf, static_cast<size_t>(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    if (reset) cudaMemset(buf, 0, 16 * sizeof(unsigned long long));
+    return n;
+}
 
 rf_status rf_zero_scalars(rf_outputs* o, void* stream) {
     if (!o || !o->scalars || !o->device_status) return RF_ERR_INVALID_ARGUMENT;
@@ -349,6 +384,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
     p.status = o->device_status;
     p.partials = ws.partials;
     p.mode = 0;
+    p.dbg = debug_counters();
 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool ib = b->logits_dtype == RF_DTYPE_BF16;
@@ -390,10 +426,10 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.nslots = g.nslots;
             const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
             const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-            const cudaError_t e = g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.nvt, g.cs, ncl, g.smem, s)
+            const cudaError_t e = g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s)
                                               : rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
             if (e != cudaSuccess) return RF_ERR_CUDA;
-            nparts = ncl;
+            nparts = g.kind == 2 ? 2 * ncl : ncl;  // lag kernel: one partial row per scalar warp
         } else {
             const int grid = generic_grid(b->num_tokens);
             if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;

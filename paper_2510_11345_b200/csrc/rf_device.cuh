@@ -58,6 +58,25 @@ struct KParams {
     int32_t nchunks;      // chunks per slice
     int32_t nslots;       // ring slots
     int32_t mode;         // 0 = fused loss+dlogits, 1 = stats only (lse/lp), 2 = write with known lse/coef
+    unsigned long long* dbg;  // optional per-phase cycle counters (RF_DEBUG_COUNTERS), else nullptr
+};
+
+// Per-phase cycle counters are compiled in only for the profiling build
+// (make PHASE=1 -> librf_offpolicy_phase.so).
+#ifndef RF_PHASE_COUNTERS
+#define RF_PHASE_COUNTERS 0
+#endif
+constexpr bool kPhaseCounters = RF_PHASE_COUNTERS != 0;
+
+// Debug phase timer: accumulates clock64 deltas into a per-thread slot array.
+struct PhaseClock {
+    long long t;
+    __device__ __forceinline__ void start() { t = clock64(); }
+    __device__ __forceinline__ void lap(unsigned long long& acc) {
+        const long long n = clock64();
+        acc += static_cast<unsigned long long>(n - t);
+        t = n;
+    }
 };
 
 // ---------------------------------------------------------------------------
@@ -107,6 +126,25 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
+}
+// Poll with a nanosleep back-off: for single-lane roles (TMA producer, scalar
+// warp) that share an SMSP with compute warps and must not steal issue slots.
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, uint32_t ns) {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-issuing polls.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity), "r"(1000000u)
+            : "memory");
+    } while (!ok);
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
     while (!mbar_try_wait_cluster(bar, parity)) {

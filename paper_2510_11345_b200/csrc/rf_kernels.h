@@ -18,19 +18,30 @@ __host__ __device__ constexpr int ring_min_blocks(int ncw) { return ncw <= kRing
 __host__ __device__ constexpr int ring_vpc(int nvt) { return nvt >= 9 ? 3 : 2; }  // vectors/thread/TMA chunk
 constexpr size_t ring_chunk_bytes(int ncw, int nvt) { return static_cast<size_t>(ncw) * 32 * ring_vpc(nvt) * 16; }
 constexpr size_t kRingTailBytes = 512;  // exchange / reduce / broadcast words
-// Lag configuration (rf_ring_lag.cu): 2 consumer warpgroups (8 warps, 224
-// registers via setmaxnreg) + a support warpgroup (TMA producer, scalar warp, 2
-// idle; 56 registers), one CTA per SM, e of the previous row parked in TMEM.
-constexpr int kRingWarpsLag = 8;
-constexpr int kRingNvtLag[3] = {4, 16, 38};
-constexpr int kLagRegsConsumer = 224;
+// Lag configuration (rf_ring_lag.cu): NCW/4 consumer warpgroups + one support
+// warpgroup (TMA producer, two scalar warps, one idle) that hands its registers to
+// the consumers via setmaxnreg; one CTA per SM; the previous row's e parked in
+// TMEM.  Default NCW = 12 (3 consumer warps per SMSP, 152 registers each).
+constexpr int kRingWarpsLag = 12;
+constexpr int kRingNvtLag[3] = {4, 12, 25};  // instances for NCW = 12
+constexpr int kRingNvtLag8 = 38;              // NCW = 8 (experiments, bf16 only)
+constexpr int kRingNvtLag16 = 19;             // NCW = 16 (experiments, bf16 only)
 constexpr int kLagRegsSupport = 56;
+__host__ __device__ constexpr int lag_launch_regs(int ncw) {
+    return ((65536 / ((ncw + 4) * 32)) / 8 * 8) > 248 ? 248 : ((65536 / ((ncw + 4) * 32)) / 8 * 8);
+}
+__host__ __device__ constexpr int lag_regs_consumer(int ncw) {
+    return ((lag_launch_regs(ncw) * (ncw + 4) * 32 - 128 * kLagRegsSupport) / (ncw * 32)) / 8 * 8 > 248
+               ? 248
+               : ((lag_launch_regs(ncw) * (ncw + 4) * 32 - 128 * kLagRegsSupport) / (ncw * 32)) / 8 * 8;
+}
+__host__ __device__ constexpr unsigned lag_tmem_cols(int ncw) { return (512u / (ncw / 4)) / 8 * 8; }
 constexpr size_t kRingLagTailBytes = 768;
 constexpr size_t kRingLagBarrierBytes = 48;
 
-cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int nvt, int cs, int nclusters,
+cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
                             size_t smem, cudaStream_t st);
-cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int nvt, int cs, size_t smem, int* out);
+cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);
 constexpr int kGenericThreads = 256;
 constexpr int kGenericMaxGrid = 148 * 8;
 

@@ -80,8 +80,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
     constexpr uint32_t CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr size_t OES = OUT_BF16 ? 2 : 4;
     constexpr size_t IES = IN_BF16 ? 2 : 4;
-    static_assert(NVT * 4 <= 256, "a thread's e values must fit its 256 TMEM columns");
-    static_assert(NCW == 8, "two consumer warpgroups (TMEM lane quarters x 2 column halves)");
+    static_assert(NCW % 4 == 0 && NCW >= 4 && NCW <= 16, "whole consumer warpgroups");
+    constexpr uint32_t TCOLS = lag_tmem_cols(NCW);  // TMEM columns per consumer warp
+    static_assert(NVT * 4 <= static_cast<int>(TCOLS), "a thread's e values must fit its TMEM columns");
+    constexpr int REGS_C = lag_regs_consumer(NCW);
 
     // smem: [nslots chunks][full][empty][x(2)][red(2)][bc(2)] + tail
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -151,12 +153,20 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             const uint64_t pol = l2_evict_first_policy();
             int s = 0;
             uint32_t phase = 0, uses = 0;
+            unsigned long long dw = 0, dt = 0;
+            PhaseClock pc;
+            pc.start();
+            const long long t_begin = pc.t;
             for (int64_t t = cid; t < p.T; t += ncl) {
                 const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
                 const uint8_t* src = reinterpret_cast<const uint8_t*>(p.logits) + (row * p.row_stride) * IES +
                                      static_cast<size_t>(slice_begin) * 16;
                 for (int c = 0; c < nchunks; ++c) {
-                    if (uses >= static_cast<uint32_t>(nslots)) mbar_wait(bar_empty + 8 * s, phase);
+                    if (uses >= static_cast<uint32_t>(nslots)) {
+                        if (kPhaseCounters && p.dbg) pc.start();
+                        mbar_wait_backoff(bar_empty + 8 * s, phase, 256);
+                        if (kPhaseCounters && p.dbg) pc.lap(dw);
+                    }
                     const int nv = min(CHUNK_VECS, slice_len - c * CHUNK_VECS);
                     const uint32_t bytes = static_cast<uint32_t>(nv) * 16;
                     mbar_arrive_expect_tx(bar_full + 8 * s, bytes);
@@ -169,15 +179,28 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     }
                 }
             }
+            if (kPhaseCounters && p.dbg) {
+                dt = static_cast<unsigned long long>(clock64() - t_begin);
+                atomicAdd(p.dbg + 10, dw);
+                atomicAdd(p.dbg + 11, dt);
+            }
         }
         __syncwarp();
-    } else if (warp == NCW + 1) {
+    } else if (warp == NCW + 1 || warp == NCW + 2) {
         // --------------------------------- scalar ---------------------------------
+        // Two scalar warps: warp NCW+1 owns the even rows of this cluster, NCW+2 the
+        // odd ones (row parity == buffer parity), so each has two rows of
+        // streaming to finish its exchange + fp64 math.
         if (lane == 0) {
+            const uint32_t which = static_cast<uint32_t>(warp - NCW - 1);
             Partials part;
             part.zero();
-            uint32_t row_iter = 0;
-            for (int64_t t = cid; t < p.T; t += ncl, ++row_iter) {
+            uint32_t row_iter = which;
+            unsigned long long d_red = 0, d_x = 0, d_math = 0;
+            PhaseClock pc;
+            pc.start();
+            const long long t_begin = pc.t;
+            for (int64_t t = cid + static_cast<int64_t>(which) * ncl; t < p.T; t += 2 * ncl, row_iter += 2) {
                 const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
                 const int32_t tok = p.token_ids[t];
                 const bool tok_ok = tok >= 0 && tok < p.V;
@@ -185,7 +208,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 const TokenPre pre = token_pre(p, t, p.seq_of_token[t]);
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
-                mbar_wait(bar_red + 8 * par, ph);
+                if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                mbar_wait_backoff(bar_red + 8 * par, ph, 128);
+                if (kPhaseCounters && p.dbg) pc.lap(d_red);
                 const float Mw = bc->ctaM;
                 const double Sw = bc->ctaS;
                 double Mc = static_cast<double>(Mw), Sc = Sw;
@@ -201,7 +226,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                         if (q == rank) continue;
                         mbar_arrive_remote(mapa(bar_x + 8 * par, q));
                     }
+                    if (kPhaseCounters && p.dbg) pc.lap(d_math);
                     mbar_wait_cluster(bar_x + 8 * par, ph);
+                    if (kPhaseCounters && p.dbg) pc.lap(d_x);
                     float Mx = -CUDART_INF_F;
                     for (uint32_t q = 0; q < csize; ++q) Mx = fmaxf(Mx, (q == rank) ? Mw : xM[par * 8 + q]);
                     Sc = 0.0;
@@ -240,8 +267,15 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     if (p.token_flags) p.token_flags[t] = static_cast<uint8_t>(tr.flags);
                     part.add_token(tr, 0.0);
                 }
+                if (kPhaseCounters && p.dbg) pc.lap(d_math);
             }
-            if (rank == 0) part.store(p.partials + static_cast<size_t>(cid) * RF_NUM_SCALARS);
+            if (rank == 0) part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
+            if (kPhaseCounters && p.dbg) {
+                atomicAdd(p.dbg + 6, d_red);
+                atomicAdd(p.dbg + 7, d_x);
+                atomicAdd(p.dbg + 8, d_math);
+                atomicAdd(p.dbg + 9, static_cast<unsigned long long>(clock64() - t_begin));
+            }
         }
         __syncwarp();
         }
@@ -250,13 +284,13 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         cluster_sync_all();
         return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kLagRegsConsumer));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_C));
     {
         // -------------------------------- consumers --------------------------------
         int s = 0;
         uint32_t fphase = 0;
         const uint64_t L2 = pk2(1.4426950408889634f, 1.4426950408889634f);
-        const uint32_t tm = tmem_base + ((32u * (warp & 3)) << 16) + 256u * (warp >> 2);
+        const uint32_t tm = tmem_base + ((32u * (warp & 3)) << 16) + TCOLS * (warp >> 2);
         uint4 r[NVT];
         // Thread-constant geometry: vector j of this thread is slice vector
         // sv(j) = (j/VPC)·CHUNK_VECS + (j%VPC)·NCT + tid, increasing in j, so the valid
@@ -271,13 +305,21 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 tail_j = (svt / CHUNK_VECS) * VPC + (svt % CHUNK_VECS) / NCT;
         }
         const size_t thr_off = static_cast<size_t>(slice_begin + tid) * EPV * OES;
+        // debug phase counters: full-wait, stream, park, coef-wait, write, total
+        unsigned long long dph[6] = {0, 0, 0, 0, 0, 0};
+        PhaseClock pcc;
+        pcc.start();
+        const long long t_begin = pcc.t;
+        const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
 
         // copy-in + max + exp sweep + CTA reduction of row t into r[]; returns C_t.
         auto stream_row = [&](uint32_t row_iter) -> float {
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
                 if (c < nchunks) {
-                    mbar_wait(bar_full + 8 * s, fphase);
+                    if (dbg) pcc.lap(dph[1]);
+                    mbar_wait_sleep(bar_full + 8 * s, fphase);
+                    if (dbg) pcc.lap(dph[0]);
                     const uint32_t slot = sbase + s * CHUNK_BYTES;
 #pragma unroll
                     for (int jj = 0; jj < VPC; ++jj) {
@@ -359,13 +401,16 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     mbar_arrive(bar_red + 8 * par);
                 }
             }
+            if (dbg) pcc.lap(dph[1]);
             return C;
         };
 
-        // write the dlogits row t (coefficient of row_iter) from registers or TMEM
+        // write the dlogits row t (coefficient of row_iter) from TMEM
         auto write_row = [&](int64_t t, uint32_t row_iter, float C) {
             const uint32_t par = row_iter & 1;
-            mbar_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
+            if (dbg) pcc.lap(dph[4]);
+            mbar_wait_sleep(bar_bc + 8 * par, (row_iter >> 1) & 1);
+            if (dbg) pcc.lap(dph[3]);
             const Bcast* bc = bcs + par;
             const float lseL = bc->lseL;
             const float negk = bc->negk;
@@ -376,24 +421,33 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             const uint64_t f2 = pk2(f, f);
             uint8_t* drow = reinterpret_cast<uint8_t*>(p.dlogits) + static_cast<size_t>(t) * p.dl_stride * OES;
             uint8_t* dthr = drow + thr_off;
+            // A rolled loop (e comes from TMEM, not from indexed registers): keeps the
+            // hot code small enough for the instruction caches.
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c) {
+                uint4 e[VPC];
+                if (c * VPC + VPC <= NVT) {
+                    if (VPC == 3) {
+                        tmem_ld8(tm + 4 * (c * VPC), e[0], e[1]);
+                        tmem_ld4(tm + 4 * (c * VPC + 2), e[VPC - 1]);
+                    } else {
+                        tmem_ld8(tm + 4 * (c * VPC), e[0], e[VPC - 1]);
+                    }
+                } else {
 #pragma unroll
-            for (int j = 0; j < NVT; j += 2) {
-                uint4 e0, e1;
-                if (j + 1 < NVT)
-                    tmem_ld8(tm + 4 * j, e0, e1);
-                else
-                    tmem_ld4(tm + 4 * j, e0);
+                    for (int h = 0; h < VPC; ++h)
+                        if (c * VPC + h < NVT) tmem_ld4(tm + 4 * (c * VPC + h), e[h]);
+                }
+                uint8_t* dc = dthr + static_cast<size_t>(c) * CHUNK_VECS * EPV * OES;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int jj = j + h;
-                    if (jj >= NVT) break;
-                    const uint4& e = h ? e1 : e0;
+                for (int h = 0; h < VPC; ++h) {
+                    const int jj = c * VPC + h;
                     if (jj < jmax) {
-                        uint8_t* dst = dthr + static_cast<size_t>((jj / VPC) * CHUNK_VECS + (jj % VPC) * NCT) * EPV * OES;
+                        uint8_t* dst = dc + static_cast<size_t>(h) * NCT * EPV * OES;
                         if (jj != tail_j)
-                            store_vec<OUT_BF16, EPV>(dst, e, f2, IN_BF16);
+                            store_vec<OUT_BF16, EPV>(dst, e[h], f2, IN_BF16);
                         else
-                            store_vec_partial<OUT_BF16, EPV>(dst, e, f, IN_BF16, tail_valid);
+                            store_vec_partial<OUT_BF16, EPV>(dst, e[h], f, IN_BF16, tail_valid);
                     }
                 }
             }
@@ -406,6 +460,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                         reinterpret_cast<float*>(drow)[tokv] = tv;
                 }
             }
+            if (dbg) pcc.lap(dph[4]);
         };
 
         uint32_t it = 0;
@@ -417,6 +472,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
 #pragma unroll
             for (int j = 0; j < NVT; ++j) tmem_st4(tm + 4 * j, r[j]);
             tmem_wait_st();
+            if (dbg) pcc.lap(dph[2]);
             const int64_t tn = t + ncl;
             float Cn = 0.f;
             if (tn < p.T) Cn = stream_row(it + 1);
@@ -424,6 +480,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             C = Cn;
             t = tn;
             ++it;
+        }
+        if (dbg) {
+            dph[5] = static_cast<unsigned long long>(clock64() - t_begin);
+            for (int q = 0; q < 6; ++q) atomicAdd(p.dbg + q, dph[q]);
         }
     }
     tmem_fence_before();
@@ -435,15 +495,15 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
 
 namespace {
 
-template <bool IB, bool OB, int NVT>
+template <bool IB, bool OB, int NCW, int NVT>
 cudaError_t launch_lag_t(const KParams& p, int cs, int nclusters, size_t smem, cudaStream_t st, int* maxc) {
-    auto kern = ring_lag_kernel<IB, OB, kRingWarpsLag, NVT>;
+    auto kern = ring_lag_kernel<IB, OB, NCW, NVT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>((maxc ? 148 : nclusters) * cs));
-    cfg.blockDim = dim3((kRingWarpsLag + 4) * 32);
+    cfg.blockDim = dim3((NCW + 4) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -458,33 +518,38 @@ cudaError_t launch_lag_t(const KParams& p, int cs, int nclusters, size_t smem, c
 }
 
 template <bool IB, bool OB>
-cudaError_t lag_nvt(const KParams& p, int nvt, int cs, int ncl, size_t smem, cudaStream_t st, int* maxc) {
-    switch (nvt) {
-        case 4: return launch_lag_t<IB, OB, 4>(p, cs, ncl, smem, st, maxc);
-        case 16: return launch_lag_t<IB, OB, 16>(p, cs, ncl, smem, st, maxc);
-        case 38: return launch_lag_t<IB, OB, 38>(p, cs, ncl, smem, st, maxc);
+cudaError_t lag_cfg(const KParams& p, int ncw, int nvt, int cs, int ncl, size_t smem, cudaStream_t st, int* maxc) {
+    if (ncw == kRingWarpsLag) {
+        switch (nvt) {
+            case kRingNvtLag[0]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[0]>(p, cs, ncl, smem, st, maxc);
+            case kRingNvtLag[1]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[1]>(p, cs, ncl, smem, st, maxc);
+            case kRingNvtLag[2]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[2]>(p, cs, ncl, smem, st, maxc);
+        }
     }
+    if (IB && OB && ncw == 8 && nvt == kRingNvtLag8) return launch_lag_t<IB, OB, 8, kRingNvtLag8>(p, cs, ncl, smem, st, maxc);
+    if (IB && OB && ncw == 16 && nvt == kRingNvtLag16)
+        return launch_lag_t<IB, OB, 16, kRingNvtLag16>(p, cs, ncl, smem, st, maxc);
     return cudaErrorInvalidValue;
 }
 
-cudaError_t lag_dispatch(const KParams& p, bool ib, bool ob, int nvt, int cs, int ncl, size_t smem, cudaStream_t st,
-                         int* maxc) {
-    if (ib && ob) return lag_nvt<true, true>(p, nvt, cs, ncl, smem, st, maxc);
-    if (ib && !ob) return lag_nvt<true, false>(p, nvt, cs, ncl, smem, st, maxc);
-    if (!ib && ob) return lag_nvt<false, true>(p, nvt, cs, ncl, smem, st, maxc);
-    return lag_nvt<false, false>(p, nvt, cs, ncl, smem, st, maxc);
+cudaError_t lag_dispatch(const KParams& p, bool ib, bool ob, int ncw, int nvt, int cs, int ncl, size_t smem,
+                         cudaStream_t st, int* maxc) {
+    if (ib && ob) return lag_cfg<true, true>(p, ncw, nvt, cs, ncl, smem, st, maxc);
+    if (ib && !ob) return lag_cfg<true, false>(p, ncw, nvt, cs, ncl, smem, st, maxc);
+    if (!ib && ob) return lag_cfg<false, true>(p, ncw, nvt, cs, ncl, smem, st, maxc);
+    return lag_cfg<false, false>(p, ncw, nvt, cs, ncl, smem, st, maxc);
 }
 
 }  // namespace
 
-cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int nvt, int cs, int nclusters,
+cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
                             size_t smem, cudaStream_t st) {
-    return lag_dispatch(p, in_bf16, out_bf16, nvt, cs, nclusters, smem, st, nullptr);
+    return lag_dispatch(p, in_bf16, out_bf16, ncw, nvt, cs, nclusters, smem, st, nullptr);
 }
 
-cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int nvt, int cs, size_t smem, int* out) {
+cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out) {
     KParams p{};
-    return lag_dispatch(p, in_bf16, out_bf16, nvt, cs, 0, smem, nullptr, out);
+    return lag_dispatch(p, in_bf16, out_bf16, ncw, nvt, cs, 0, smem, nullptr, out);
 }
 
 }  // namespace rf

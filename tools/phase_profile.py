@@ -1,0 +1,48 @@
+"""Per-phase cycle breakdown of the fused kernel (run on the GPU box):
+    RF_DEBUG_COUNTERS=1 python tools/phase_profile.py [--prompts 32]
+Prints, per consumer warp, where the cycles of one launch went."""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2510_11345_b200 as rf  # noqa: E402
+from paper_2510_11345_b200 import _abi, synth as S  # noqa: E402
+from paper_2510_11345_b200 import losses as L  # noqa: E402
+from tests.cases import config  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--prompts", type=int, default=32)
+ap.add_argument("--variant", default="decoupled_ppo")
+a = ap.parse_args()
+assert os.environ.get("RF_DEBUG_COUNTERS") == "1"
+wl = S.WORKLOADS["c2"]
+rb = S.make_rank_batch(wl, 0, 1, 42, a.prompts)
+dw = S.DeviceWorkload(rb, wl.vocab, pool_gb=8, device="cuda")
+pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_offsets, advantages=dw.advantages,
+                   behavior_logp=dw.behavior_logp, row_of_token=dw.row_of_token, prox_logp=dw.prox_logp,
+                   engine_logp=dw.engine_logp, normalization=L.Normalization.global_token)
+op = rf.OffPolicyLoss(config(a.variant), pb, chunk_tokens=min(65536, dw.T))
+lib = _abi.load_library()
+buf = np.zeros(16, dtype=np.uint64)
+for rep in range(3):
+    op.zero()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    op.run(pb, 0, op.chunk)
+    ev1.record()
+    torch.cuda.synchronize()
+    lib.rf_debug_counters(buf.ctypes.data, 16, 1)
+ms = ev0.elapsed_time(ev1)
+names = ["cons.full_wait", "cons.stream", "cons.park", "cons.coef_wait", "cons.write", "cons.total",
+         "scal.red_wait", "scal.peer_wait", "scal.math", "scal.total", "prod.empty_wait", "prod.total"]
+ncta = 148
+print(f"launch {ms:.3f} ms for {op.chunk} tokens -> {op.chunk * 4 * wl.vocab / ms / 1e6:.1f} GB/s")
+cons_warps = ncta * 8
+for i, n in enumerate(names):
+    div = cons_warps if n.startswith("cons") else (ncta * 2 if n.startswith("scal") else ncta)
+    print(f"{n:18s} {buf[i] / div / 1e3:10.1f} kcycles per warp   ({buf[i] / max(buf[5 if n.startswith('cons') else (9 if n.startswith('scal') else 11)], 1) * 100:5.1f}%)")
