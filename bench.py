@@ -231,7 +231,7 @@ def impl_reference(args, wl, variant):
 # ---------------------------------------------------------------------------
 # Our arm
 # ---------------------------------------------------------------------------
-def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1):
+def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1, chunk=1024):
     """The reference-facing C-ABI call with HOST buffers (rf_loss_and_grad_host):
     pinned host logits rows in, pinned host dlogits + per-token outputs + scalars
     out; every H2D/D2H copy is inside the timed region."""
@@ -287,7 +287,6 @@ def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1):
     o.scalars, o.device_status = h_scal.data_ptr(), h_status.data_ptr()
     lib = _abi.load_library()
     dev = torch.cuda.current_device()
-    chunk = 2048
     for _ in range(warmup):
         st = lib.rf_loss_and_grad_host(ctypes.byref(cfg), ctypes.byref(b), ctypes.byref(o), dev, chunk)
         assert st == 0, L.status_string(st)

@@ -66,6 +66,10 @@ def ref_available() -> bool:
     return os.path.exists(REF_SO)
 
 
+GPU_SHIM_SO = os.path.join(os.path.dirname(_HERE), "integration", "_build", "librlsim_gpu.so")
+_shim = None
+
+
 def ref_lib():
     global _ref
     if _ref is None:
@@ -73,7 +77,25 @@ def ref_lib():
             build()
         if not os.path.exists(REF_SO):
             raise OSError("oracle/_ref/librlsim_ref.so not built (reference sources absent)")
-        L = ctypes.CDLL(REF_SO)
+        _ref = _bind(ctypes.CDLL(REF_SO))
+    return _ref
+
+
+def gpu_shim_available() -> bool:
+    return os.path.exists(GPU_SHIM_SO)
+
+
+def gpu_shim_lib():
+    """The reference's own code (bandit/policy/rng/engine/gradcheck) linked against
+    integration/rlsim_gpu_shim.cpp — rlsim's loss API on the GPU (integration/Makefile)."""
+    global _shim
+    if _shim is None:
+        _shim = _bind(ctypes.CDLL(GPU_SHIM_SO))
+    return _shim
+
+
+def _bind(L):
+    if True:
         L.ref_grpo_advantages.restype = _i32
         L.ref_grpo_advantages.argtypes = [_P, _i64, _P, _P, ctypes.c_char_p, ctypes.c_int]
         L.ref_variant_from_string.restype = _i32
@@ -102,8 +124,7 @@ def ref_lib():
                                      _P, _P, _P, _P, _P, _P, ctypes.c_char_p, ctypes.c_int]
         L.ref_rng_draws.restype = None
         L.ref_rng_draws.argtypes = [ctypes.c_uint64, ctypes.c_char_p, _i32, _i64, _P]
-        _ref = L
-    return _ref
+    return L
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -217,7 +238,7 @@ def ref_validate(cfg) -> Optional[str]:
 
 
 def ref_loss_and_grad(cfg, logits, traj_context, traj_offsets, tokens, advantages, behavior_logp, *,
-                      prox_logits=None, ref_logits=None, engine_logp=None, want_grad=True):
+                      prox_logits=None, ref_logits=None, engine_logp=None, want_grad=True, lib=None):
     """rlsim::loss_and_grad over trajectories; logits [C, V] fp64.  Returns (value, grad) or raises."""
     lg = _c(logits, np.float64)
     C, V = lg.shape
@@ -233,7 +254,7 @@ def ref_loss_and_grad(cfg, logits, traj_context, traj_offsets, tokens, advantage
     val = np.zeros(1)
     e = _err()
     p = config_params(cfg)
-    st = ref_lib().ref_loss_and_grad(int(cfg.variant), int(cfg.aggregation), _ptr(p), C, V, _ptr(lg), _ptr(prox),
+    st = (lib or ref_lib()).ref_loss_and_grad(int(cfg.variant), int(cfg.aggregation), _ptr(p), C, V, _ptr(lg), _ptr(prox),
                                      _ptr(ref), len(ctx), _ptr(ctx), _ptr(offs), _ptr(tok), _ptr(adv), _ptr(beh),
                                      _ptr(eng), _ptr(val), _ptr(grad), e, 512)
     if st:
@@ -293,7 +314,7 @@ def ref_bench_mapping_a(cfg, logits, tokens, advantages, behavior_logp, *, prox_
 
 
 def ref_train_loop(cfg, *, contexts=4, arms=10, group_size=8, traj_len=1, steps=200, lr=0.5, reward_noise=0.0,
-                   async_lag=0, seed=0):
+                   async_lag=0, seed=0, lib=None):
     p = config_params(cfg)
     fr = np.zeros(1)
     gv = np.zeros(1)
@@ -301,7 +322,7 @@ def ref_train_loop(cfg, *, contexts=4, arms=10, group_size=8, traj_len=1, steps=
     cg = np.zeros(steps)
     cs = np.zeros(steps, dtype=np.int64)
     e = _err()
-    if ref_lib().ref_train_loop(contexts, arms, group_size, traj_len, steps, lr, reward_noise, async_lag, seed,
+    if (lib or ref_lib()).ref_train_loop(contexts, arms, group_size, traj_len, steps, lr, reward_noise, async_lag, seed,
                                 int(cfg.variant), int(cfg.aggregation), _ptr(p), _ptr(fr), _ptr(gv), _ptr(cr),
                                 _ptr(cg), _ptr(cs), e, 512):
         raise ValueError(e.value.decode())

@@ -88,6 +88,15 @@ extern "C" rf_status rf_loss_and_grad_host(const rf_loss_config* c, const rf_bat
     const size_t row_bytes = static_cast<size_t>(hb->logits_row_stride) * les;
     const size_t drow_bytes = static_cast<size_t>(ho->dlogits_row_stride) * des;
 
+    // Keep the stream-ordered pool's memory mapped between calls (the default
+    // release threshold of 0 returns it to the OS at every synchronisation).
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     cudaStream_t s_h2d, s_cmp, s_d2h;
     cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&s_cmp, cudaStreamNonBlocking);

@@ -78,6 +78,7 @@ def main():
                 out[key + "/behavior"] = case.behavior_logp
                 out[key + "/engine"] = case.engine_logp
                 out[key + "/prox_logp"] = lq
+                out[key + "/prox_table"] = prox_tab
                 if case.ref_logits is not None:
                     out[key + "/ref_logits"] = case.ref_logits
                 if rows is not None:
