@@ -231,22 +231,30 @@ def _stream_handle(stream) -> int:
     return stream.cuda_stream
 
 
-def grpo_advantages(rewards: torch.Tensor, group_offsets: torch.Tensor, stream=None):
+def grpo_advantages(rewards: torch.Tensor, group_offsets: torch.Tensor, stream=None, *, out=None,
+                    validate: bool = True):
     """K1 — rlsim::grpo_advantages (losses.cpp:41-60) over CSR groups on the GPU.
 
     Returns (advantages f64 [N], degenerate uint8 [G]).  Bit-identical to the
-    reference.  Raises InvalidArgument for a group smaller than 2.
+    reference.  Raises InvalidArgument for a group smaller than 2 (``validate``
+    reads the offsets on the host; a training loop validates its batch layout
+    once and passes ``validate=False`` plus preallocated ``out=(adv, deg,
+    status)`` to keep the step free of host syncs and allocations).
     """
     G = int(group_offsets.numel() - 1)
     if G <= 0:
         raise InvalidArgument("grpo_advantages: group size must be >= 2")
-    sizes = (group_offsets[1:] - group_offsets[:-1])
-    if bool((sizes < 2).any()):
-        raise InvalidArgument("grpo_advantages: group size must be >= 2")
+    if validate:
+        sizes = (group_offsets[1:] - group_offsets[:-1])
+        if bool((sizes < 2).any()):
+            raise InvalidArgument("grpo_advantages: group size must be >= 2")
     dev = rewards.device
-    adv = torch.empty_like(rewards, dtype=torch.float64)
-    deg = torch.empty(G, dtype=torch.uint8, device=dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    if out is not None:
+        adv, deg, status = out
+    else:
+        adv = torch.empty_like(rewards, dtype=torch.float64)
+        deg = torch.empty(G, dtype=torch.uint8, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
     b = rf_batch()
     b.num_groups = G
     b.num_seqs = int(rewards.numel())
