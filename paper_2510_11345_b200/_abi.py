@@ -11,9 +11,10 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# RF_LIB_VARIANT=phase loads the profiling build (per-phase cycle counters compiled in).
-LIB_PATH = os.path.join(_HERE, "librf_offpolicy_phase.so" if os.environ.get("RF_LIB_VARIANT") == "phase"
-                        else "librf_offpolicy.so")
+# RF_LIB_VARIANT=<name> loads an experiment build librf_offpolicy_<name>.so (e.g. "phase":
+# per-phase cycle counters compiled in; see the Makefile's `variant` target).
+_VARIANT = os.environ.get("RF_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, f"librf_offpolicy_{_VARIANT}.so" if _VARIANT else "librf_offpolicy.so")
 
 # enums (rf_offpolicy.h)
 RF_PPO, RF_DECOUPLED_PPO, RF_TIS, RF_CISPO, RF_TOPR, RF_GRPO, RF_NAIVE_IS = range(7)

@@ -103,7 +103,8 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
             }
         }
         if (!nvt) continue;
-        const size_t cb = rf::ring_chunk_bytes(ncw, nvt);
+        const size_t cb = g.kind == 2 ? static_cast<size_t>(ncw) * 32 * rf::lag_vpc(nvt) * 16
+                                      : rf::ring_chunk_bytes(ncw, nvt);
         g.cs = cs;
         g.ncw = ncw;
         g.nvt = nvt;

@@ -196,6 +196,16 @@ __device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
 __device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
+// Release-store to a peer CTA's shared memory / acquire-load of a local word at
+// cluster scope (sequence-number handshakes).
+__device__ __forceinline__ void st_release_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+    asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -335,7 +345,7 @@ __device__ __forceinline__ double token_scale_of(const KParams& p, int64_t seq) 
 // The lp-independent half of the per-token math (loads + the theta-constant
 // factors), computed while the row's softmax is still being reduced.
 struct TokenPre {
-    double b, lq, A, scale, m, po;
+    double b, lq, A, scale, m, po, eb;  // eb = exp(b)
     uint32_t flags;
 };
 
@@ -343,6 +353,7 @@ __device__ __forceinline__ TokenPre token_pre(const KParams& p, int64_t t, int64
     TokenPre q;
     q.flags = 0;
     q.b = load_logp(p.behavior_logp, t, p.logp_f64);
+    q.eb = exp(q.b);
     q.A = p.advantages[seq];
     q.scale = token_scale_of(p, seq);
     q.m = 1.0;

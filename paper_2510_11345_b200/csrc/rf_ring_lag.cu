@@ -30,6 +30,27 @@ using namespace ring;
 
 namespace {
 
+// Lanes of each scalar warp taking part in the per-row combine (32: shuffle
+// tree; 1: lane 0 alone).  Build-time knob for A/B runs (make variant).
+#ifndef RF_SCALAR_LANES
+#define RF_SCALAR_LANES 1
+#endif
+constexpr int kScalarLanes = RF_SCALAR_LANES;
+// Producer back-off while the ring is full (ns; 0 = spin) and the consumers' wait
+// flavour (1 = try_wait with a suspend-time hint, 0 = spin) — A/B knobs.
+#ifndef RF_PROD_SLEEP_NS
+#define RF_PROD_SLEEP_NS 256
+#endif
+#ifndef RF_CONS_SUSPEND
+#define RF_CONS_SUSPEND 1
+#endif
+__device__ __forceinline__ void cons_wait(uint32_t bar, uint32_t parity) {
+    if (RF_CONS_SUSPEND)
+        mbar_wait_sleep(bar, parity);
+    else
+        mbar_wait(bar, parity);
+}
+
 __device__ __forceinline__ void tmem_alloc(uint32_t smem_dst, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst), "r"(ncols)
                  : "memory");
@@ -59,6 +80,61 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint4& a, uint4& b) {
         : "r"(taddr), "r"(taddr + 4)
         : "memory");
 }
+// N consecutive 4-column loads (N 16-byte vectors of this thread) and one wait.
+template <int N>
+__device__ __forceinline__ void tmem_ld_vecs(uint32_t taddr, uint4* e) {
+    static_assert(N >= 1 && N <= 5, "1..5 vectors per call");
+
+    if constexpr (N == 1) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n\t"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(e[0].x), "=r"(e[0].y), "=r"(e[0].z), "=r"(e[0].w)
+            : "r"(taddr)
+            : "memory");
+    } else if constexpr (N == 2) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%8];\n\t"
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%9];\n\t"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(e[0].x), "=r"(e[0].y), "=r"(e[0].z), "=r"(e[0].w), "=r"(e[1].x), "=r"(e[1].y), "=r"(e[1].z),
+              "=r"(e[1].w)
+            : "r"(taddr), "r"(taddr + 4)
+            : "memory");
+    } else if constexpr (N == 3) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%12];\n\t"
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%13];\n\t"
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8, %9, %10, %11}, [%14];\n\t"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(e[0].x), "=r"(e[0].y), "=r"(e[0].z), "=r"(e[0].w), "=r"(e[1].x), "=r"(e[1].y), "=r"(e[1].z),
+              "=r"(e[1].w), "=r"(e[2].x), "=r"(e[2].y), "=r"(e[2].z), "=r"(e[2].w)
+            : "r"(taddr), "r"(taddr + 4), "r"(taddr + 8)
+            : "memory");
+    } else if constexpr (N == 4) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];\n\t"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(e[0].x), "=r"(e[0].y), "=r"(e[0].z), "=r"(e[0].w), "=r"(e[1].x), "=r"(e[1].y), "=r"(e[1].z),
+              "=r"(e[1].w), "=r"(e[2].x), "=r"(e[2].y), "=r"(e[2].z), "=r"(e[2].w), "=r"(e[3].x), "=r"(e[3].y),
+              "=r"(e[3].z), "=r"(e[3].w)
+            : "r"(taddr)
+            : "memory");
+    } else {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%20];\n\t"
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%16, %17, %18, %19}, [%21];\n\t"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(e[0].x), "=r"(e[0].y), "=r"(e[0].z), "=r"(e[0].w), "=r"(e[1].x), "=r"(e[1].y), "=r"(e[1].z),
+              "=r"(e[1].w), "=r"(e[2].x), "=r"(e[2].y), "=r"(e[2].z), "=r"(e[2].w), "=r"(e[3].x), "=r"(e[3].y),
+              "=r"(e[3].z), "=r"(e[3].w), "=r"(e[4].x), "=r"(e[4].y), "=r"(e[4].z), "=r"(e[4].w)
+            : "r"(taddr), "r"(taddr + 16)
+            : "memory");
+    }
+
+}
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint4& a) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n\t"
@@ -74,7 +150,7 @@ template <bool IN_BF16, bool OUT_BF16, int NCW, int NVT>
 __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __grid_constant__ KParams p) {
     constexpr int NCT = NCW * 32;
     constexpr int EPV = IN_BF16 ? 8 : 4;
-    constexpr int VPC = ring_vpc(NVT);
+    constexpr int VPC = lag_vpc(NVT);
     constexpr int NCH = (NVT + VPC - 1) / VPC;
     constexpr int CHUNK_VECS = NCT * VPC;
     constexpr uint32_t CHUNK_BYTES = CHUNK_VECS * 16;
@@ -91,14 +167,21 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar_full = sbase + nslots * CHUNK_BYTES;
     const uint32_t bar_empty = bar_full + nslots * 8;
-    const uint32_t bar_x = bar_empty + nslots * 8;  // [2] cluster exchange (row parity)
-    const uint32_t bar_red = bar_x + 16;             // [2] consumers -> scalar: CTA partial (row parity)
+    const uint32_t bar_red = bar_empty + nslots * 8 + 16;  // [2] consumers -> scalar: CTA partial (row parity)
     const uint32_t bar_bc = bar_red + 16;            // [2] scalar -> consumers: coefficient (row parity)
     uint8_t* tail = smem + nslots * CHUNK_BYTES + nslots * 16 + 48;
-    double* xS = reinterpret_cast<double*>(tail);              // [2][8]
-    float* xM = reinterpret_cast<float*>(tail + 128);          // [2][8]
-    double* redS = reinterpret_cast<double*>(tail + 192);      // [2][NCW]
-    float* redM = reinterpret_cast<float*>(tail + 192 + 16 * NCW);  // [2][NCW]
+    // Cluster exchange slots [row % 4][sender rank]: written remotely by the peer's
+    // scalar warp, guarded by a sequence word (row + 1) instead of an mbarrier phase,
+    // so a peer running ahead can never alias a phase (a peer is at most one row of
+    // the same parity ahead, and 4 slots cover it).
+    struct XSlot {
+        double S;
+        float M;
+        uint32_t seq;
+    };
+    XSlot* xslot = reinterpret_cast<XSlot*>(tail);                  // [4][8]
+    double* redS = reinterpret_cast<double*>(tail + 512);           // [2][NCW]
+    float* redM = reinterpret_cast<float*>(tail + 512 + 16 * NCW);  // [2][NCW]
     struct Bcast {
         double ctaS;
         float ctaM, lseL;
@@ -106,7 +189,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         float negk;
         int32_t tok;
     };
-    Bcast* bcs = reinterpret_cast<Bcast*>(tail + 192 + 24 * NCW + ((24 * NCW) % 8 ? 4 : 0));  // [2]
+    Bcast* bcs = reinterpret_cast<Bcast*>(tail + 512 + 24 * NCW + ((24 * NCW) % 8 ? 4 : 0));  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bcs + 2);
 
     const int tid = threadIdx.x;
@@ -122,10 +205,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             mbar_init(bar_empty + 8 * s, NCW);
         }
         for (int q = 0; q < 2; ++q) {
-            mbar_init(bar_x + 8 * q, csize > 1 ? csize - 1 : 1);
-            mbar_init(bar_red + 8 * q, 1);
+            mbar_init(bar_red + 8 * q, NCW);  // one arrival per consumer warp partial
             mbar_init(bar_bc + 8 * q, 1);
         }
+        for (int q = 0; q < 32; ++q) xslot[q].seq = 0u;
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -164,7 +247,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 for (int c = 0; c < nchunks; ++c) {
                     if (uses >= static_cast<uint32_t>(nslots)) {
                         if (kPhaseCounters && p.dbg) pc.start();
-                        mbar_wait_backoff(bar_empty + 8 * s, phase, 256);
+                        if (RF_PROD_SLEEP_NS > 0)
+                            mbar_wait_backoff(bar_empty + 8 * s, phase, RF_PROD_SLEEP_NS);
+                        else
+                            mbar_wait(bar_empty + 8 * s, phase);
                         if (kPhaseCounters && p.dbg) pc.lap(dw);
                     }
                     const int nv = min(CHUNK_VECS, slice_len - c * CHUNK_VECS);
@@ -191,7 +277,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         // Two scalar warps: warp NCW+1 owns the even rows of this cluster, NCW+2 the
         // odd ones (row parity == buffer parity), so each has two rows of
         // streaming to finish its exchange + fp64 math.
-        if (lane == 0) {
+        {
             const uint32_t which = static_cast<uint32_t>(warp - NCW - 1);
             Partials part;
             part.zero();
@@ -201,40 +287,74 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             pc.start();
             const long long t_begin = pc.t;
             for (int64_t t = cid + static_cast<int64_t>(which) * ncl; t < p.T; t += 2 * ncl, row_iter += 2) {
-                const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
-                const int32_t tok = p.token_ids[t];
-                const bool tok_ok = tok >= 0 && tok < p.V;
-                const float x_tok = tok_ok ? load_logit(p.logits, row * p.row_stride + tok, IN_BF16) : 0.0f;
-                const TokenPre pre = token_pre(p, t, p.seq_of_token[t]);
+                if (kScalarLanes == 1 && lane != 0) break;
+                int32_t tok = -1;
+                bool tok_ok = false;
+                float x_tok = 0.0f;
+                TokenPre pre{};
+                if (lane == 0) {  // issue the per-token loads before waiting
+                    const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
+                    tok = p.token_ids[t];
+                    tok_ok = tok >= 0 && tok < p.V;
+                    x_tok = tok_ok ? load_logit(p.logits, row * p.row_stride + tok, IN_BF16) : 0.0f;
+                    pre = token_pre(p, t, p.seq_of_token[t]);
+                }
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
                 mbar_wait_backoff(bar_red + 8 * par, ph, 128);
                 if (kPhaseCounters && p.dbg) pc.lap(d_red);
-                const float Mw = bc->ctaM;
-                const double Sw = bc->ctaS;
+                float Mw;
+                double Sw;
+                if constexpr (kScalarLanes > 1) {
+                    // combine the consumer warps' partials across the scalar warp's lanes
+                    // (fixed shuffle tree: deterministic)
+                    const float Mq = lane < NCW ? redM[par * NCW + lane] : -CUDART_INF_F;
+                    const double Sq = lane < NCW ? redS[par * NCW + lane] : 0.0;
+                    Mw = Mq;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
+                    Sw = (Sq != 0.0) ? Sq * exp2(static_cast<double>(Mq) - static_cast<double>(Mw)) : 0.0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) Sw += __shfl_xor_sync(0xffffffffu, Sw, o);
+                    if (lane != 0) {  // park at the row's closing __syncwarp (no polling)
+                        __syncwarp();
+                        continue;
+                    }
+                } else {  // lane 0 alone, sequential in warp order
+                    Mw = -CUDART_INF_F;
+                    for (int w = 0; w < NCW; ++w) Mw = fmaxf(Mw, redM[par * NCW + w]);
+                    Sw = 0.0;
+                    for (int w = 0; w < NCW; ++w) {
+                        const double sw = redS[par * NCW + w];
+                        if (sw != 0.0)
+                            Sw += sw * exp2(static_cast<double>(redM[par * NCW + w]) - static_cast<double>(Mw));
+                    }
+                }
                 double Mc = static_cast<double>(Mw), Sc = Sw;
                 if (csize > 1) {
-                    const uint32_t myS = smem_u32(&xS[par * 8 + rank]);
-                    const uint32_t myM = smem_u32(&xM[par * 8 + rank]);
-                    for (uint32_t q = 0; q < csize; ++q) {
+                    const uint32_t slot = (row_iter & 3) * 8 + rank;
+                    XSlot* mine = &xslot[slot];
+                    for (uint32_t q = 0; q < csize; ++q) {  // push (S, M) to every peer, then publish
                         if (q == rank) continue;
-                        st_cluster_f64(mapa(myS, q), Sw);
-                        st_cluster_f32(mapa(myM, q), Mw);
-                    }
-                    for (uint32_t q = 0; q < csize; ++q) {
-                        if (q == rank) continue;
-                        mbar_arrive_remote(mapa(bar_x + 8 * par, q));
+                        st_cluster_f64(mapa(smem_u32(&mine->S), q), Sw);
+                        st_cluster_f32(mapa(smem_u32(&mine->M), q), Mw);
+                        st_release_cluster_u32(mapa(smem_u32(&mine->seq), q), row_iter + 1);
                     }
                     if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                    mbar_wait_cluster(bar_x + 8 * par, ph);
+                    for (uint32_t q = 0; q < csize; ++q) {  // wait for every peer's partial of this row
+                        if (q == rank) continue;
+                        const uint32_t a = smem_u32(&xslot[(row_iter & 3) * 8 + q].seq);
+                        while (ld_acquire_cluster_u32(a) != row_iter + 1) __nanosleep(32);
+                    }
                     if (kPhaseCounters && p.dbg) pc.lap(d_x);
                     float Mx = -CUDART_INF_F;
-                    for (uint32_t q = 0; q < csize; ++q) Mx = fmaxf(Mx, (q == rank) ? Mw : xM[par * 8 + q]);
+                    for (uint32_t q = 0; q < csize; ++q)
+                        Mx = fmaxf(Mx, (q == rank) ? Mw : xslot[(row_iter & 3) * 8 + q].M);
                     Sc = 0.0;
                     for (uint32_t q = 0; q < csize; ++q) {  // rank order: identical on every CTA
-                        const float Mq = (q == rank) ? Mw : xM[par * 8 + q];
-                        const double Sq = (q == rank) ? Sw : xS[par * 8 + q];
+                        const float Mq = (q == rank) ? Mw : xslot[(row_iter & 3) * 8 + q].M;
+                        const double Sq = (q == rank) ? Sw : xslot[(row_iter & 3) * 8 + q].S;
                         if (Sq != 0.0) Sc += Sq * exp2(static_cast<double>(Mq) - static_cast<double>(Mx));
                     }
                     Mc = static_cast<double>(Mx);
@@ -254,7 +374,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     if (tr.flags & RF_FLAG_NONFINITE) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
                 }
                 bc->k = tr.k;
-                bc->tok_val = (tok_ok && tr.k != 0.0) ? tr.k - tr.k * exp(lp) : 0.0;
+                // p_tok = exp(lp) = ratio · exp(b) (exp(b) precomputed while waiting)
+                bc->tok_val = (tok_ok && tr.k != 0.0) ? tr.k - tr.k * (tr.ratio * pre.eb) : 0.0;
                 bc->lseL = static_cast<float>(lse * 1.4426950408889634);
                 bc->negk = static_cast<float>(-tr.k);
                 bc->tok = tok_ok ? tok : -1;
@@ -268,9 +389,11 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     part.add_token(tr, 0.0);
                 }
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                if constexpr (kScalarLanes > 1) __syncwarp();
             }
-            if (rank == 0) part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
-            if (kPhaseCounters && p.dbg) {
+            if (lane == 0 && rank == 0)
+                part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
+            if (kPhaseCounters && p.dbg && lane == 0) {
                 atomicAdd(p.dbg + 6, d_red);
                 atomicAdd(p.dbg + 7, d_x);
                 atomicAdd(p.dbg + 8, d_math);
@@ -318,7 +441,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             for (int c = 0; c < NCH; ++c) {
                 if (c < nchunks) {
                     if (dbg) pcc.lap(dph[1]);
-                    mbar_wait_sleep(bar_full + 8 * s, fphase);
+                    cons_wait(bar_full + 8 * s, fphase);
                     if (dbg) pcc.lap(dph[0]);
                     const uint32_t slot = sbase + s * CHUNK_BYTES;
 #pragma unroll
@@ -373,7 +496,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 S += static_cast<double>(lo2(acc) + hi2(acc));
             }
             const float Mr = (S == 0.0) ? -CUDART_INF_F : C;
-            // CTA reduction of (C, S) pairs in the log2 domain -> scalar warp
+            // warp reduction of (C, S) pairs in the log2 domain; each warp hands its
+            // partial straight to the scalar warp (no CTA-wide barrier on the consumers)
             const uint32_t par = row_iter & 1;
             float Mw = Mr;
 #pragma unroll
@@ -384,22 +508,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             if (lane == 0) {
                 redM[par * NCW + warp] = Mw;
                 redS[par * NCW + warp] = sw;
-            }
-            named_bar_sync(1, NCT);
-            if (warp == 0) {
-                const float Mq = lane < NCW ? redM[par * NCW + lane] : -CUDART_INF_F;
-                const double Sq = lane < NCW ? redS[par * NCW + lane] : 0.0;
-                float Mx = Mq;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
-                double sx = (Sq != 0.0) ? Sq * exp2(static_cast<double>(Mq) - static_cast<double>(Mx)) : 0.0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
-                if (lane == 0) {
-                    bcs[par].ctaM = Mx;
-                    bcs[par].ctaS = sx;
-                    mbar_arrive(bar_red + 8 * par);
-                }
+                mbar_arrive(bar_red + 8 * par);  // release: the scalar warp's wait sees the words above
             }
             if (dbg) pcc.lap(dph[1]);
             return C;
@@ -409,7 +518,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         auto write_row = [&](int64_t t, uint32_t row_iter, float C) {
             const uint32_t par = row_iter & 1;
             if (dbg) pcc.lap(dph[4]);
-            mbar_wait_sleep(bar_bc + 8 * par, (row_iter >> 1) & 1);
+            cons_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
             if (dbg) pcc.lap(dph[3]);
             const Bcast* bc = bcs + par;
             const float lseL = bc->lseL;
@@ -427,12 +536,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             for (int c = 0; c < NCH; ++c) {
                 uint4 e[VPC];
                 if (c * VPC + VPC <= NVT) {
-                    if (VPC == 3) {
-                        tmem_ld8(tm + 4 * (c * VPC), e[0], e[1]);
-                        tmem_ld4(tm + 4 * (c * VPC + 2), e[VPC - 1]);
-                    } else {
-                        tmem_ld8(tm + 4 * (c * VPC), e[0], e[VPC - 1]);
-                    }
+                    tmem_ld_vecs<VPC>(tm + 4 * (c * VPC), e);  // VPC loads, one wait
                 } else {
 #pragma unroll
                     for (int h = 0; h < VPC; ++h)
