@@ -401,7 +401,24 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
         p.token_logp = o->token_logp ? o->token_logp : ws.lp;
         const int grid = generic_grid(b->num_tokens);
         p.mode = 1;
-        if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
+        // Fast path: stats pass on the cluster ring kernel (lse per token, one read of
+        // the logits), sequence scalars, then the streaming dlogits pass — 6·V bytes
+        // per token.  Exact-KL and unaligned layouts take the generic kernel.
+        RingGeometry g;
+        if (kernel != RF_KERNEL_GENERIC && !needs_ref) g = ring_geometry(b, o);
+        if (kernel == RF_KERNEL_RING && !g.ok) return RF_ERR_UNSUPPORTED_LAYOUT;
+        if (g.ok && g.kind == 2) {
+            p.slice_vecs = g.slice_vecs;
+            p.row_vecs = g.row_vecs;
+            p.nchunks = g.nchunks;
+            p.nslots = g.nslots;
+            const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
+            const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
+            if (rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s) != cudaSuccess)
+                return RF_ERR_CUDA;
+        } else {
+            if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
+        }
         if (rf::launch_seq(p, 0, b->num_seqs, ws.coef, s) != cudaSuccess) return RF_ERR_CUDA;
         if (o->token_coef)
             if (cudaMemcpyAsync(o->token_coef, ws.coef, static_cast<size_t>(b->num_tokens) * 8,
@@ -413,7 +430,9 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             KParams q = p;
             q.mode = 2;
             q.token_coef = ws.coef;
-            if (rf::launch_generic(q, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
+            const cudaError_t e = (g.ok && g.kind == 2) ? rf::launch_stream_write(q, ib, ob, s)
+                                                         : rf::launch_generic(q, ib, ob, grid, s);
+            if (e != cudaSuccess) return RF_ERR_CUDA;
             g_last_launches += 1;
         }
     } else {

@@ -54,6 +54,8 @@ cudaError_t launch_ring(const KParams& p, bool in_bf16, bool out_bf16, int ncw, 
                         size_t smem, cudaStream_t st);
 cudaError_t ring_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);
 cudaError_t launch_generic(const KParams& p, bool in_bf16, bool out_bf16, int grid, cudaStream_t st);
+// K2w (rf_stream.cu): dlogits from per-token coef + lse (needs p.row_vecs, ring-compatible layout)
+cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st);
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st);
 cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, cudaStream_t st);
 cudaError_t launch_grpo(const double* rewards, const int64_t* group_offsets, int64_t num_groups, double* adv,

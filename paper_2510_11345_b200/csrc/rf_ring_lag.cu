@@ -360,6 +360,15 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     Mc = static_cast<double>(Mx);
                 }
                 const double lse = 0.69314718055994530942 * (Mc + log2(Sc));  // natural-log lse
+                if (p.mode == 1) {  // stats pass (sequence_product): lse and lp per token only
+                    if (rank == 0) {
+                        p.tok_lse[t] = lse;
+                        p.token_logp[t] = tok_ok ? static_cast<double>(x_tok) - lse : CUDART_NAN;
+                        if (!tok_ok) atomicOr(p.status, RF_DEVSTAT_TOKEN_OUT_OF_RANGE);
+                    }
+                    mbar_arrive(bar_bc + 8 * par);  // keeps the consumers' row pacing
+                    continue;
+                }
                 TokenResult tr;
                 double lp = CUDART_NAN;
                 if (!tok_ok) {
@@ -520,6 +529,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             if (dbg) pcc.lap(dph[4]);
             cons_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
             if (dbg) pcc.lap(dph[3]);
+            if (p.mode == 1) return;  // stats pass: no dlogits
             const Bcast* bc = bcs + par;
             const float lseL = bc->lseL;
             const float negk = bc->negk;
@@ -574,7 +584,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         while (t < p.T) {
             // park e_t in TMEM, stream row t + ncl (if any), then write row t from TMEM
 #pragma unroll
-            for (int j = 0; j < NVT; ++j) tmem_st4(tm + 4 * j, r[j]);
+            for (int j = 0; j < NVT; ++j)
+                if (p.mode != 1) tmem_st4(tm + 4 * j, r[j]);
             tmem_wait_st();
             if (dbg) pcc.lap(dph[2]);
             const int64_t tn = t + ncl;

@@ -206,3 +206,26 @@ def test_missing_inputs_raise():
     pb.engine_logp = None
     with pytest.raises(rf.InvalidArgument, match="engine"):
         rf.loss_and_grad(_cfg("tis", cap=5.0), pb)
+
+
+@pytest.mark.parametrize("variant", ["ppo", "tis", "topr", "cispo", "decoupled_ppo", "naive_is"])
+@pytest.mark.parametrize("V", [32000, 151936])
+def test_sequence_product_fast_path(variant, V):
+    """Ring stats pass + sequence scalars + streaming dlogits pass (ring-compatible layout)."""
+    case = make_case(25, T_seqs=8, G=4, V=V, max_len=6, mapping="A", stale=0.05)
+    cfg = _cfg(variant, aggregation="sequence_product")
+    pb = to_device_batch(case, normalization=L.Normalization.seq_then_batch)
+    gpu = rf.loss_and_grad(cfg, pb, kernel="ring")
+    ref = run_oracle(case, cfg, normalization=0)
+    compare(case, cfg, gpu, ref)
+    gen = rf.loss_and_grad(cfg, pb, kernel="generic")
+    assert torch.equal(gpu.token_flags, gen.token_flags)
+
+
+def test_sequence_product_mapping_b_fast_path():
+    case = make_case(26, T_seqs=12, G=4, V=32000, max_len=9, mapping="B", stale=0.1)
+    cfg = _cfg("tis", aggregation="sequence_product")
+    pb = to_device_batch(case)
+    gpu = rf.loss_and_grad(cfg, pb, kernel="ring")
+    ref = run_oracle(case, cfg, normalization=0)
+    compare(case, cfg, gpu, ref)
