@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--variant", default=None)
+    ap.add_argument("--aggregation", default="token_mean", choices=["token_mean", "sequence_product"])
     ap.add_argument("--prompts", type=int, default=None, help="prompts per rank (default: the config's)")
     ap.add_argument("--chunk-tokens", type=int, default=65536)
     ap.add_argument("--pool-gb", type=float, default=48.0)
@@ -321,30 +322,34 @@ def impl_ours(args, wl, variant):
         dist.init_process_group("nccl", device_id=dev)
     rb = S.make_rank_batch(wl, rank, world, 42, args.prompts)
     dw = S.DeviceWorkload(rb, wl.vocab, pool_gb=args.pool_gb, device=dev, seed=42 + rank)
-    cfg = config(variant)
+    cfg = config(variant, aggregation=args.aggregation)
     pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_offsets,
                        advantages=dw.advantages, behavior_logp=dw.behavior_logp, row_of_token=dw.row_of_token,
                        prox_logp=dw.prox_logp, engine_logp=dw.engine_logp, rewards=dw.rewards,
                        group_offsets=dw.group_offsets, normalization=L.Normalization.global_token,
                        global_num_seqs=rb.global_seqs, global_num_tokens=rb.global_tokens)
     chunk = min(args.chunk_tokens, dw.T)
-    op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=chunk, kernel=args.kernel)
     stream = torch.cuda.current_stream()
-    chunks = [(t0, min(dw.T, t0 + chunk)) for t0 in range(0, dw.T, chunk)]
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in chunks]
-
     rf.grpo_advantages(pb.rewards, pb.group_offsets, stream)  # validates the group layout once
     k1_out = (torch.empty_like(pb.rewards), torch.empty(dw.group_offsets.numel() - 1, dtype=torch.uint8, device=dev),
               torch.zeros(1, dtype=torch.int32, device=dev))
+    pb.advantages = k1_out[0]
+    if args.aggregation == "sequence_product":
+        # whole sequences per call (the sequence weights need every token's log-prob)
+        calls = [(0, t1 - t0, sub, t0) for t0, t1, sub in pb.sequence_chunks(chunk)]
+        chunk = max(c[1] for c in calls)
+    else:
+        calls = [(t0, min(dw.T, t0 + chunk), pb, t0) for t0 in range(0, dw.T, chunk)]
+    op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=chunk, kernel=args.kernel)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in calls]
 
     def step(record=False):
-        adv, _ = rf.grpo_advantages(pb.rewards, pb.group_offsets, stream, out=k1_out, validate=False)
-        pb.advantages = adv
+        rf.grpo_advantages(pb.rewards, pb.group_offsets, stream, out=k1_out, validate=False)
         op.zero(stream)
-        for i, (t0, t1) in enumerate(chunks):
+        for i, (t0, t1, b, out_t0) in enumerate(calls):
             if record:
                 ev[i][0].record(stream)
-            op.run(pb, t0, t1, stream)
+            op.run(b, t0, t1, stream, out_t0=out_t0)
             if record:
                 ev[i][1].record(stream)
         if world > 1:
@@ -387,16 +392,20 @@ def impl_ours(args, wl, variant):
     value = tokens_global / (ms_step / 1e3)
 
     peak, peak_kind = load_peaks()
-    bytes_tok = 4 * wl.vocab
+    seqprod = args.aggregation == "sequence_product"
+    # token_mean: one read + one write of each row (4V B/token); sequence_product: a
+    # stats read pass + a read/write dlogits pass (6V B/token)
+    bytes_tok = (6 if seqprod else 4) * wl.vocab
     # achieved bandwidth of the dominant kernel: algorithmic bytes / kernel time (last step)
     achieved = dw.T * bytes_tok / (kern_ms / 1e3) / 1e9
-    tpt = traffic_per_token(wl.vocab)
-    launch_tokens = chunks[0][1] - chunks[0][0]
+    tpt = None if seqprod else traffic_per_token(wl.vocab)
+    launch_tokens = calls[0][1] - calls[0][0]
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None if tpt is None else int(tpt * launch_tokens),
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, torch bf16 copy)" if peak_kind == "measured"
             else "fallback 6.65 TB/s (B200_PROFILING.md)",
-            "kernel": "ring_kernel (K2, incl. its K3 finalize launch)",
+            "kernel": ("ring_lag_kernel stats pass + seq_kernel + stream_write_kernel (+K3)" if seqprod
+                       else "ring_lag_kernel (K2, incl. its K3 finalize launch)"),
             "algorithmic_bytes_per_token": bytes_tok, "tokens_per_launch": launch_tokens,
             "kernel_ms_per_step": round(kern_ms, 3)}
 
@@ -418,7 +427,8 @@ def impl_ours(args, wl, variant):
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": wl.description, "variant": variant, "vocab": wl.vocab,
+            "config": {"workload": wl.description, "variant": variant, "aggregation": args.aggregation,
+                       "vocab": wl.vocab,
                        "prompts_per_gpu": args.prompts or wl.prompts, "group": wl.group, "max_len": wl.max_len,
                        "async_ratio": wl.alpha, "tokens_per_gpu": dw.T, "tokens_global": tokens_global,
                        "chunk_tokens": chunk, "logits_pool_rows": dw.pool_rows,

@@ -168,6 +168,35 @@ class PackedBatch:
     def num_seqs(self) -> int:
         return int(self.seq_offsets.numel() - 1)
 
+    def sequence_chunks(self, max_tokens: int):
+        """Split into calls of whole sequences (sequence_product needs every token of
+        a sequence in one call).  Yields (t0, t1, sub_batch): the sub-batch views the
+        token arrays [t0, t1), the sequence arrays of its sequences, and has
+        ``seq_of_token`` rebased to them; global normalisers are kept."""
+        offs = self.seq_offsets.cpu().tolist()
+        N = len(offs) - 1
+        s = 0
+        while s < N:
+            e = s + 1
+            while e < N and offs[e + 1] - offs[s] <= max_tokens:
+                e += 1
+            t0, t1 = offs[s] - offs[0], offs[e] - offs[0]
+            sub = PackedBatch(
+                logits=self.logits if self.row_of_token is not None else self.logits[t0:t1],
+                token_ids=self.token_ids[t0:t1], seq_offsets=self.seq_offsets[s:e + 1],
+                advantages=None if self.advantages is None else self.advantages[s:e],
+                behavior_logp=self.behavior_logp[t0:t1], vocab=self.vocab,
+                seq_of_token=self.seq_of_token[t0:t1] - s,
+                row_of_token=None if self.row_of_token is None else self.row_of_token[t0:t1],
+                prox_logp=None if self.prox_logp is None else self.prox_logp[t0:t1],
+                engine_logp=None if self.engine_logp is None else self.engine_logp[t0:t1],
+                ref_logits=(self.ref_logits if (self.ref_logits is None or self.row_of_token is not None)
+                            else self.ref_logits[t0:t1]),
+                normalization=self.normalization, global_num_seqs=self.global_num_seqs,
+                global_num_tokens=self.global_num_tokens, grad_sign=self.grad_sign)
+            yield t0, t1, sub
+            s = e
+
     def to_c(self, t0: int = 0, t1: Optional[int] = None) -> rf_batch:
         """rf_batch for the token range [t0, t1) (a streaming chunk)."""
         T = self.num_tokens
@@ -327,12 +356,16 @@ class OffPolicyLoss:
         o = self.outputs_c(0)
         _raise_for(_lib().rf_zero_scalars(ctypes.byref(o), _stream_handle(stream)))
 
-    def run(self, batch: PackedBatch, t0: int = 0, t1: Optional[int] = None, stream=None) -> None:
+    def run(self, batch: PackedBatch, t0: int = 0, t1: Optional[int] = None, stream=None,
+            out_t0: Optional[int] = None) -> None:
+        """Tokens [t0, t1) of ``batch``; per-token outputs land at ``out_t0`` (default t0)
+        of the preallocated arrays (a sequence chunk from ``sequence_chunks`` passes its
+        own offset)."""
         t1 = batch.num_tokens if t1 is None else t1
         if t1 - t0 > self.chunk:
             raise InvalidArgument("chunk larger than the preallocated dlogits buffer")
         b = batch.to_c(t0, t1)
-        o = self.outputs_c(t0)
+        o = self.outputs_c(t0 if out_t0 is None else out_t0)
         lib = _lib()
         _raise_for(lib.rf_loss_and_grad_ex(ctypes.byref(self.cfg_c), ctypes.byref(b), ctypes.byref(o),
                                            _stream_handle(stream), self.kernel))

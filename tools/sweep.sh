@@ -1,0 +1,12 @@
+#!/bin/bash
+# All BASELINE.json configs on one GPU (run on the GPU box): gpurun_out/sweep_<name>.log
+mkdir -p gpurun_out
+run() { name=$1; shift; timeout 900 python bench.py --no-e2e --no-cpu-baseline "$@" > gpurun_out/sweep_$name.log 2>&1; echo "$name rc=$?" >> gpurun_out/sweep_rc.log; }
+rm -f gpurun_out/sweep_rc.log
+run c1 --workload c1 --steps 5 --warmup 3
+run c2 --workload c2 --steps 5 --warmup 3
+run c3_tis --workload c3 --variant tis --steps 3 --warmup 2
+run c3_topr --workload c3 --variant topr --steps 3 --warmup 2
+run c4 --workload c4 --steps 3 --warmup 2
+run c2_seqprod --workload c2 --aggregation sequence_product --steps 3 --warmup 2
+run c5 --workload c5 --steps 2 --warmup 1 --pool-gb 64
