@@ -50,6 +50,21 @@ __device__ __forceinline__ void cons_wait(uint32_t bar, uint32_t parity) {
     else
         mbar_wait(bar, parity);
 }
+// Support-warp waits (producer empty slots, scalar partials): 1 = suspend-hint
+// try_wait, 0 = nanosleep polling (each poll costs issue slots on a consumer SMSP).
+#ifndef RF_SUPPORT_SUSPEND
+#define RF_SUPPORT_SUSPEND 1  // A/B on B200: +2% over 128 ns polling
+#endif
+__device__ __forceinline__ void support_wait(uint32_t bar, uint32_t parity, uint32_t ns) {
+    if (RF_SUPPORT_SUSPEND)
+        mbar_wait_sleep(bar, parity);
+    else
+        mbar_wait_backoff(bar, parity, ns);
+}
+// Write phase: straight-line stores for chunks with no padded / missing vectors.
+#ifndef RF_WRITE_FAST
+#define RF_WRITE_FAST 1  // A/B on B200: +6% (per-vector branches serialised the store math)
+#endif
 
 __device__ __forceinline__ void tmem_alloc(uint32_t smem_dst, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst), "r"(ncols)
@@ -248,7 +263,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     if (uses >= static_cast<uint32_t>(nslots)) {
                         if (kPhaseCounters && p.dbg) pc.start();
                         if (RF_PROD_SLEEP_NS > 0)
-                            mbar_wait_backoff(bar_empty + 8 * s, phase, RF_PROD_SLEEP_NS);
+                            support_wait(bar_empty + 8 * s, phase, RF_PROD_SLEEP_NS);
                         else
                             mbar_wait(bar_empty + 8 * s, phase);
                         if (kPhaseCounters && p.dbg) pc.lap(dw);
@@ -302,7 +317,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                mbar_wait_backoff(bar_red + 8 * par, ph, 128);
+                support_wait(bar_red + 8 * par, ph, 128);
                 if (kPhaseCounters && p.dbg) pc.lap(d_red);
                 float Mw;
                 double Sw;
@@ -436,6 +451,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             if (svt >= 0 && svt < slice_len && (svt % CHUNK_VECS) % NCT == tid)
                 tail_j = (svt / CHUNK_VECS) * VPC + (svt % CHUNK_VECS) / NCT;
         }
+        const int jfull = tail_j >= 0 ? tail_j : jmax;  // j < jfull: complete vectors (tail_j == jmax - 1)
         const size_t thr_off = static_cast<size_t>(slice_begin + tid) * EPV * OES;
         // debug phase counters: full-wait, stream, park, coef-wait, write, total
         unsigned long long dph[6] = {0, 0, 0, 0, 0, 0};
@@ -553,6 +569,12 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                         if (c * VPC + h < NVT) tmem_ld4(tm + 4 * (c * VPC + h), e[h]);
                 }
                 uint8_t* dc = dthr + static_cast<size_t>(c) * CHUNK_VECS * EPV * OES;
+                if (RF_WRITE_FAST && c * VPC + VPC <= jfull) {
+#pragma unroll
+                    for (int h = 0; h < VPC; ++h)
+                        store_vec<OUT_BF16, EPV>(dc + static_cast<size_t>(h) * NCT * EPV * OES, e[h], f2, IN_BF16);
+                    continue;
+                }
 #pragma unroll
                 for (int h = 0; h < VPC; ++h) {
                     const int jj = c * VPC + h;
