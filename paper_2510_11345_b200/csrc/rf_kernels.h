@@ -26,7 +26,10 @@ constexpr int kRingWarpsLag = 12;
 constexpr int kRingNvtLag[3] = {4, 12, 25};  // instances for NCW = 12
 constexpr int kRingNvtLag8 = 38;              // NCW = 8 (experiments, bf16 only)
 constexpr int kRingNvtLag16 = 19;             // NCW = 16 (experiments, bf16 only)
-constexpr int kLagRegsSupport = 56;
+#ifndef RF_LAG_REGS_SUPPORT
+#define RF_LAG_REGS_SUPPORT 56  // support warpgroup registers (A/B knob: 32 gives the consumers 160)
+#endif
+constexpr int kLagRegsSupport = RF_LAG_REGS_SUPPORT;
 __host__ __device__ constexpr int lag_launch_regs(int ncw) {
     return ((65536 / ((ncw + 4) * 32)) / 8 * 8) > 248 ? 248 : ((65536 / ((ncw + 4) * 32)) / 8 * 8);
 }
