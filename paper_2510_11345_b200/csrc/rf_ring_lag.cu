@@ -67,6 +67,18 @@ __device__ __forceinline__ void support_wait(uint32_t bar, uint32_t parity, uint
 #ifndef RF_PARK_MODE
 #define RF_PARK_MODE 2  // A/B on B200: +1.5% over 0, +1% over 1
 #endif
+// Rescale factor 2^(m - mx) (m <= mx, log2 domain) of a partial softmax sum when
+// partials are combined.  RF_FAST_COMBINE (A/B knob): 1 = MUFU ex2 of the exact
+// (fp64) difference, relative error ~2^-22 — the class of every element's own
+// ex2.approx — instead of a ~200-cycle fp64 exp2 on the per-row critical path.
+#ifndef RF_FAST_COMBINE
+#define RF_FAST_COMBINE 1  // A/B on B200: +6.3% (the per-lane fp64 exp2 sat on every warp's row path)
+#endif
+__device__ __forceinline__ double combine_factor(float m, float mx) {
+    const double d = static_cast<double>(m) - static_cast<double>(mx);
+    if (RF_FAST_COMBINE) return static_cast<double>(ex2_approx(static_cast<float>(d)));
+    return exp2(d);
+}
 // Write phase: straight-line stores for chunks with no padded / missing vectors.
 #ifndef RF_WRITE_FAST
 #define RF_WRITE_FAST 1  // A/B on B200: +6% (per-vector branches serialised the store math)
@@ -335,7 +347,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     Mw = Mq;
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
-                    Sw = (Sq != 0.0) ? Sq * exp2(static_cast<double>(Mq) - static_cast<double>(Mw)) : 0.0;
+                    Sw = (Sq != 0.0) ? Sq * combine_factor(Mq, Mw) : 0.0;
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) Sw += __shfl_xor_sync(0xffffffffu, Sw, o);
                     if (lane != 0) {  // park at the row's closing __syncwarp (no polling)
@@ -349,7 +361,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     for (int w = 0; w < NCW; ++w) {
                         const double sw = redS[par * NCW + w];
                         if (sw != 0.0)
-                            Sw += sw * exp2(static_cast<double>(redM[par * NCW + w]) - static_cast<double>(Mw));
+                            Sw += sw * combine_factor(redM[par * NCW + w], Mw);
                     }
                 }
                 double Mc = static_cast<double>(Mw), Sc = Sw;
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     for (uint32_t q = 0; q < csize; ++q) {  // rank order: identical on every CTA
                         const float Mq = (q == rank) ? Mw : xslot[(row_iter & 3) * 8 + q].M;
                         const double Sq = (q == rank) ? Sw : xslot[(row_iter & 3) * 8 + q].S;
-                        if (Sq != 0.0) Sc += Sq * exp2(static_cast<double>(Mq) - static_cast<double>(Mx));
+                        if (Sq != 0.0) Sc += Sq * combine_factor(Mq, Mx);
                     }
                     Mc = static_cast<double>(Mx);
                 }
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             float Mw = Mr;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
-            double sw = (S != 0.0) ? S * exp2(static_cast<double>(Mr) - static_cast<double>(Mw)) : 0.0;
+            double sw = (S != 0.0) ? S * combine_factor(Mr, Mw) : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sw += __shfl_xor_sync(0xffffffffu, sw, o);
             if (lane == 0) {
