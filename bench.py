@@ -341,17 +341,19 @@ def impl_ours(args, wl, variant):
     else:
         calls = [(t0, min(dw.T, t0 + chunk), pb, t0) for t0 in range(0, dw.T, chunk)]
     op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=chunk, kernel=args.kernel)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in calls]
+    # one event pair per (timed step, chunk): the kernel time is averaged over every timed step
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in calls]
+          for _ in range(args.steps)]
 
-    def step(record=False):
+    def step(record=None):
         rf.grpo_advantages(pb.rewards, pb.group_offsets, stream, out=k1_out, validate=False)
         op.zero(stream)
         for i, (t0, t1, b, out_t0) in enumerate(calls):
-            if record:
-                ev[i][0].record(stream)
+            if record is not None:
+                ev[record][i][0].record(stream)
             op.run(b, t0, t1, stream, out_t0=out_t0)
-            if record:
-                ev[i][1].record(stream)
+            if record is not None:
+                ev[record][i][1].record(stream)
         if world > 1:
             dist.all_reduce(op.scalars)
 
@@ -371,8 +373,8 @@ def impl_ours(args, wl, variant):
     launches_before = op.launches
     start.record(stream)
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ selects exactly these launches
-    for _ in range(args.steps):
-        step(record=True)
+    for k in range(args.steps):
+        step(record=k)
     torch.cuda.nvtx.range_pop()
     stop.record(stream)
     torch.cuda.synchronize()
@@ -380,9 +382,11 @@ def impl_ours(args, wl, variant):
         dist.barrier()
     clk = clocks.stop()
     ms_total = start.elapsed_time(stop)
-    # ring-kernel time over the last step's chunks (events reused per step)
-    for a, b2 in ev:
-        kern_ms += a.elapsed_time(b2)
+    # ring-kernel time per step: every chunk's launch pair, averaged over the timed steps
+    for evs in ev:
+        for a, b2 in evs:
+            kern_ms += a.elapsed_time(b2)
+    kern_ms /= args.steps
     launches = (op.launches - launches_before) + args.steps  # + one K1 per step
     t_local = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
@@ -396,7 +400,7 @@ def impl_ours(args, wl, variant):
     # token_mean: one read + one write of each row (4V B/token); sequence_product: a
     # stats read pass + a read/write dlogits pass (6V B/token)
     bytes_tok = (6 if seqprod else 4) * wl.vocab
-    # achieved bandwidth of the dominant kernel: algorithmic bytes / kernel time (last step)
+    # achieved bandwidth of the dominant kernel: algorithmic bytes / kernel time per step
     achieved = dw.T * bytes_tok / (kern_ms / 1e3) / 1e9
     tpt = None if seqprod else traffic_per_token(wl.vocab)
     launch_tokens = calls[0][1] - calls[0][0]

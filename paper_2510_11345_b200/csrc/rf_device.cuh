@@ -196,6 +196,19 @@ __device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
 __device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
+// Asynchronous store into a peer CTA's shared memory that completes `bytes` of the
+// transaction count of the peer's mbarrier (both addresses from mapa): no fence, no
+// polling — the receiver waits on its local mbarrier.
+__device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "l"(__double_as_longlong(v)), "r"(cluster_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_f32(uint32_t cluster_addr, float v, uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "r"(__float_as_uint(v)), "r"(cluster_bar)
+                 : "memory");
+}
 // Release-store to a peer CTA's shared memory / acquire-load of a local word at
 // cluster scope (sequence-number handshakes).
 __device__ __forceinline__ void st_release_cluster_u32(uint32_t cluster_addr, uint32_t v) {

@@ -44,7 +44,7 @@ __host__ __device__ constexpr unsigned lag_tmem_cols(int ncw) { return (512u / (
 #define RF_LAG_VPC 5  // 30 KB chunks at 12 consumer warps: measured best of {2,3,4,5,7,9,13}
 #endif
 __host__ __device__ constexpr int lag_vpc(int nvt) { return (RF_LAG_VPC > 0 && nvt >= 9) ? RF_LAG_VPC : ring_vpc(nvt); }
-constexpr size_t kRingLagTailBytes = 1024;
+constexpr size_t kRingLagTailBytes = 1088;  // exchange / reduce / broadcast words + 4 exchange mbarriers
 constexpr size_t kRingLagBarrierBytes = 48;
 
 cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,

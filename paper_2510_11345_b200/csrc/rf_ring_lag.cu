@@ -79,6 +79,20 @@ __device__ __forceinline__ double combine_factor(float m, float mx) {
     if (RF_FAST_COMBINE) return static_cast<double>(ex2_approx(static_cast<float>(d)));
     return exp2(d);
 }
+// Per-thread softmax sum: 0 = every vector's fp32 sum folded into fp64 (a 25-deep
+// F2F + DADD chain), 1 = four fp32 chains folded once (A/B knob).
+#ifndef RF_SUM_F32
+#define RF_SUM_F32 0
+#endif
+// Cluster exchange of the CTA partials: 1 = st.async + complete_tx on the peer's
+// mbarrier (no fence, no polling); 0 = sequence words with st.release / ld.acquire
+// polling (each poll invalidates L1, each release fences) — A/B knob.
+#ifndef RF_XCHG_MBAR
+#define RF_XCHG_MBAR 0
+#endif
+#ifndef RF_XCHG_SPIN
+#define RF_XCHG_SPIN 0  // exchange wait: 1 = try_wait polling with a 32 ns back-off
+#endif
 // Write phase: straight-line stores for chunks with no padded / missing vectors.
 #ifndef RF_WRITE_FAST
 #define RF_WRITE_FAST 1  // A/B on B200: +6% (per-vector branches serialised the store math)
@@ -213,6 +227,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         uint32_t seq;
     };
     XSlot* xslot = reinterpret_cast<XSlot*>(tail);                  // [4][8]
+    const uint32_t xbar = smem_u32(tail + 1024);                     // [4] exchange mbarriers (RF_XCHG_MBAR)
     double* redS = reinterpret_cast<double*>(tail + 512);           // [2][NCW]
     float* redM = reinterpret_cast<float*>(tail + 512 + 16 * NCW);  // [2][NCW]
     struct Bcast {
@@ -242,6 +257,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             mbar_init(bar_bc + 8 * q, 1);
         }
         for (int q = 0; q < 32; ++q) xslot[q].seq = 0u;
+        for (int q = 0; q < 4; ++q) mbar_init(xbar + 8 * q, 1);  // the local scalar's arrive.expect_tx
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -315,7 +331,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             Partials part;
             part.zero();
             uint32_t row_iter = which;
-            unsigned long long d_red = 0, d_x = 0, d_math = 0;
+            unsigned long long d_red = 0, d_x = 0, d_math = 0, d_post = 0;
             PhaseClock pc;
             pc.start();
             const long long t_begin = pc.t;
@@ -366,21 +382,42 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 }
                 double Mc = static_cast<double>(Mw), Sc = Sw;
                 if (csize > 1) {
-                    const uint32_t slot = (row_iter & 3) * 8 + rank;
-                    XSlot* mine = &xslot[slot];
-                    for (uint32_t q = 0; q < csize; ++q) {  // push (S, M) to every peer, then publish
-                        if (q == rank) continue;
-                        st_cluster_f64(mapa(smem_u32(&mine->S), q), Sw);
-                        st_cluster_f32(mapa(smem_u32(&mine->M), q), Mw);
-                        st_release_cluster_u32(mapa(smem_u32(&mine->seq), q), row_iter + 1);
+                    if (RF_XCHG_MBAR) {
+                        // st.async the (S, M) partial into every peer's slot, completing bytes
+                        // on the peer's exchange mbarrier of this row slot; then arm the local
+                        // one and wait for every peer's partial of this row
+                        const uint32_t xs = row_iter & 3;
+                        const XSlot* mine = &xslot[xs * 8 + rank];
+                        for (uint32_t q = 0; q < csize; ++q) {
+                            if (q == rank) continue;
+                            const uint32_t rb = mapa(xbar + 8 * xs, q);
+                            st_async_f64(mapa(smem_u32(&mine->S), q), Sw, rb);
+                            st_async_f32(mapa(smem_u32(&mine->M), q), Mw, rb);
+                        }
+                        mbar_arrive_expect_tx(xbar + 8 * xs, 12u * (csize - 1));
+                        if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                        if (RF_XCHG_SPIN)
+                            mbar_wait_backoff(xbar + 8 * xs, (row_iter >> 2) & 1, 32);
+                        else
+                            support_wait(xbar + 8 * xs, (row_iter >> 2) & 1, 32);
+                        if (kPhaseCounters && p.dbg) pc.lap(d_x);
+                    } else {
+                        const uint32_t slot = (row_iter & 3) * 8 + rank;
+                        XSlot* mine = &xslot[slot];
+                        for (uint32_t q = 0; q < csize; ++q) {  // push (S, M) to every peer, then publish
+                            if (q == rank) continue;
+                            st_cluster_f64(mapa(smem_u32(&mine->S), q), Sw);
+                            st_cluster_f32(mapa(smem_u32(&mine->M), q), Mw);
+                            st_release_cluster_u32(mapa(smem_u32(&mine->seq), q), row_iter + 1);
+                        }
+                        if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                        for (uint32_t q = 0; q < csize; ++q) {  // wait for every peer's partial of this row
+                            if (q == rank) continue;
+                            const uint32_t a = smem_u32(&xslot[(row_iter & 3) * 8 + q].seq);
+                            while (ld_acquire_cluster_u32(a) != row_iter + 1) __nanosleep(32);
+                        }
+                        if (kPhaseCounters && p.dbg) pc.lap(d_x);
                     }
-                    if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                    for (uint32_t q = 0; q < csize; ++q) {  // wait for every peer's partial of this row
-                        if (q == rank) continue;
-                        const uint32_t a = smem_u32(&xslot[(row_iter & 3) * 8 + q].seq);
-                        while (ld_acquire_cluster_u32(a) != row_iter + 1) __nanosleep(32);
-                    }
-                    if (kPhaseCounters && p.dbg) pc.lap(d_x);
                     float Mx = -CUDART_INF_F;
                     for (uint32_t q = 0; q < csize; ++q)
                         Mx = fmaxf(Mx, (q == rank) ? Mw : xslot[(row_iter & 3) * 8 + q].M);
@@ -422,6 +459,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 bc->negk = static_cast<float>(-tr.k);
                 bc->tok = tok_ok ? tok : -1;
                 mbar_arrive(bar_bc + 8 * par);
+                if (kPhaseCounters && p.dbg) pc.lap(d_post);  // partials in -> k published (after the peer wait)
                 if (rank == 0) {
                     if (p.token_logp) p.token_logp[t] = lp;
                     if (p.token_ratio) p.token_ratio[t] = tr.ratio;
@@ -439,6 +477,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 atomicAdd(p.dbg + 6, d_red);
                 atomicAdd(p.dbg + 7, d_x);
                 atomicAdd(p.dbg + 8, d_math);
+                atomicAdd(p.dbg + 12, d_post);
                 atomicAdd(p.dbg + 9, static_cast<unsigned long long>(clock64() - t_begin));
             }
         }
@@ -538,10 +577,24 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             const float C = Mt * 1.4426950408889634f;
             const uint64_t negC2 = pk2(-C, -C);
             double S = 0.0;
+            if (RF_SUM_F32) {  // four fp32 chains (two packed pairs), folded into fp64 once
+                uint64_t A0 = pk2(0.0f, 0.0f), A1 = pk2(0.0f, 0.0f);
 #pragma unroll
-            for (int j = 0; j < NVT; ++j) {
-                const uint64_t acc = vec_exp<IN_BF16>(r[j], L2, negC2);
-                S += static_cast<double>(lo2(acc) + hi2(acc));
+                for (int j = 0; j < NVT; ++j) {
+                    const uint64_t acc = vec_exp<IN_BF16>(r[j], L2, negC2);
+                    if (j & 1)
+                        A1 = fadd2(A1, acc);
+                    else
+                        A0 = fadd2(A0, acc);
+                }
+                S = (static_cast<double>(lo2(A0)) + static_cast<double>(hi2(A0))) +
+                    (static_cast<double>(lo2(A1)) + static_cast<double>(hi2(A1)));
+            } else {
+#pragma unroll
+                for (int j = 0; j < NVT; ++j) {
+                    const uint64_t acc = vec_exp<IN_BF16>(r[j], L2, negC2);
+                    S += static_cast<double>(lo2(acc) + hi2(acc));
+                }
             }
             const float Mr = (S == 0.0) ? -CUDART_INF_F : C;
             // warp reduction of (C, S) pairs in the log2 domain; each warp hands its

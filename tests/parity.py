@@ -12,7 +12,9 @@ Tolerances (north star, BASELINE.json):
 """
 from __future__ import annotations
 
+import json
 import math
+import os
 
 import numpy as np
 import torch
@@ -110,9 +112,20 @@ def kink_band(case, cfg, ref_out, logp_dtype=torch.float64) -> np.ndarray:
     return band
 
 
-def compare(case, cfg, gpu: L.LossResult, ref: dict, *, out_dtype=torch.bfloat16, check_dlogits=True,
-            logp_dtype=torch.float64, rows=None):
-    """Assert parity; returns a dict of observed max errors."""
+def compare(case, cfg, gpu: L.LossResult, ref: dict, **kw):
+    """Assert parity; returns a dict of observed max errors.  With RF_PARITY_LOG=<file>
+    the stats of every passing comparison are appended there as JSON lines (precision
+    reports across library variants)."""
+    stats = _compare(case, cfg, gpu, ref, **kw)
+    log = os.environ.get("RF_PARITY_LOG")
+    if log:
+        with open(log, "a") as f:
+            f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], **stats}) + "\n")
+    return stats
+
+
+def _compare(case, cfg, gpu: L.LossResult, ref: dict, *, out_dtype=torch.bfloat16, check_dlogits=True,
+             logp_dtype=torch.float64, rows=None):
     band = kink_band(case, cfg, ref, logp_dtype)
     ok = ~band
     stats = {"kink_band_tokens": int(band.sum())}

@@ -39,10 +39,11 @@ for rep in range(3):
     lib.rf_debug_counters(buf.ctypes.data, 16, 1)
 ms = ev0.elapsed_time(ev1)
 names = ["cons.full_wait", "cons.stream", "cons.park", "cons.coef_wait", "cons.write", "cons.total",
-         "scal.red_wait", "scal.peer_wait", "scal.math", "scal.total", "prod.empty_wait", "prod.total"]
+         "scal.red_wait", "scal.peer_wait", "scal.math", "scal.total", "prod.empty_wait", "prod.total",
+         "scal.post_to_k"]
 ncta = 148
 print(f"launch {ms:.3f} ms for {op.chunk} tokens -> {op.chunk * 4 * wl.vocab / ms / 1e6:.1f} GB/s")
-cons_warps = ncta * 8
+cons_warps = ncta * int(os.environ.get("RF_LAG_WARPS", "12"))
 for i, n in enumerate(names):
     div = cons_warps if n.startswith("cons") else (ncta * 2 if n.startswith("scal") else ncta)
     print(f"{n:18s} {buf[i] / div / 1e3:10.1f} kcycles per warp   ({buf[i] / max(buf[5 if n.startswith('cons') else (9 if n.startswith('scal') else 11)], 1) * 100:5.1f}%)")
