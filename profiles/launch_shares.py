@@ -8,7 +8,7 @@ rows = list(csv.reader(open(sys.argv[1])))
 start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[start]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 tot, cnt = defaultdict(float), defaultdict(int)
 for r in rows[start + 1:]:
     if len(r) <= vi:
