@@ -40,7 +40,7 @@ for rep in range(3):
 ms = ev0.elapsed_time(ev1)
 names = ["cons.full_wait", "cons.stream", "cons.park", "cons.coef_wait", "cons.write", "cons.total",
          "scal.red_wait", "scal.peer_wait", "scal.math", "scal.total", "prod.empty_wait", "prod.total",
-         "scal.post_to_k"]
+         "scal.post_to_k", "scal.post.lse", "scal.post.token_post"]
 ncta = 148
 print(f"launch {ms:.3f} ms for {op.chunk} tokens -> {op.chunk * 4 * wl.vocab / ms / 1e6:.1f} GB/s")
 cons_warps = ncta * int(os.environ.get("RF_LAG_WARPS", "12"))
