@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "ring", "generic"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-tokens", type=int, default=8192)
+    ap.add_argument("--e2e-tokens", type=int, default=16384)
     ap.add_argument("--cpu-rows", type=int, default=0, help="reference sample rows (0 = auto)")
     return ap.parse_args()
 
@@ -232,7 +232,7 @@ def impl_reference(args, wl, variant):
 # ---------------------------------------------------------------------------
 # Our arm
 # ---------------------------------------------------------------------------
-def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1, chunk=1024):
+def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1, chunk=512):
     """The reference-facing C-ABI call with HOST buffers (rf_loss_and_grad_host):
     pinned host logits rows in, pinned host dlogits + per-token outputs + scalars
     out; every H2D/D2H copy is inside the timed region."""
