@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--chunk-tokens", type=int, default=65536)
     ap.add_argument("--pool-gb", type=float, default=48.0)
     ap.add_argument("--kernel", default="auto", choices=["auto", "ring", "generic"])
+    ap.add_argument("--kl-weight", type=float, default=0.0,
+                    help="exact-KL GRPO (variant grpo, a reference-policy row per token, 6·V B/token)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-tokens", type=int, default=16384)
@@ -322,8 +324,20 @@ def impl_ours(args, wl, variant):
         dist.init_process_group("nccl", device_id=dev)
     rb = S.make_rank_batch(wl, rank, world, 42, args.prompts)
     dw = S.DeviceWorkload(rb, wl.vocab, pool_gb=args.pool_gb, device=dev, seed=42 + rank)
-    cfg = config(variant, aggregation=args.aggregation)
-    pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_offsets,
+    cfg = config(variant, aggregation=args.aggregation, kl_weight=args.kl_weight)
+    ref_pool = None
+    if args.kl_weight > 0:
+        # exact-KL GRPO: a second, independent pool of reference-policy rows (π_ref),
+        # indexed by the same row_of_token, so every token reads both rows from HBM
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(4242 + rank)
+        full = torch.empty(dw.pool_rows, (wl.vocab + 7) // 8 * 8, dtype=torch.bfloat16, device=dev)
+        step = max(1, int(2e9 // (full.shape[1] * 4)))
+        for r0 in range(0, dw.pool_rows, step):
+            r1 = min(dw.pool_rows, r0 + step)
+            full[r0:r1].copy_(torch.randn(r1 - r0, full.shape[1], generator=gen, device=dev) * 2.0)
+        ref_pool = full[:, : wl.vocab]
+    pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_offsets, ref_logits=ref_pool,
                        advantages=dw.advantages, behavior_logp=dw.behavior_logp, row_of_token=dw.row_of_token,
                        prox_logp=dw.prox_logp, engine_logp=dw.engine_logp, rewards=dw.rewards,
                        group_offsets=dw.group_offsets, normalization=L.Normalization.global_token,
@@ -399,16 +413,18 @@ def impl_ours(args, wl, variant):
     seqprod = args.aggregation == "sequence_product"
     # token_mean: one read + one write of each row (4V B/token); sequence_product: a
     # stats read pass + a read/write dlogits pass (6V B/token)
-    bytes_tok = (6 if seqprod else 4) * wl.vocab
+    bytes_tok = (6 if (seqprod or args.kl_weight > 0) else 4) * wl.vocab  # + the π_ref row read
     # achieved bandwidth of the dominant kernel: algorithmic bytes / kernel time per step
     achieved = dw.T * bytes_tok / (kern_ms / 1e3) / 1e9
-    tpt = None if seqprod else traffic_per_token(wl.vocab)
+    kl = args.kl_weight > 0
+    tpt = None if (seqprod or kl) else traffic_per_token(wl.vocab)
     launch_tokens = calls[0][1] - calls[0][0]
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None if tpt is None else int(tpt * launch_tokens),
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, torch bf16 copy)" if peak_kind == "measured"
             else "fallback 6.65 TB/s (B200_PROFILING.md)",
             "kernel": ("ring_lag_kernel stats pass + seq_kernel + stream_write_kernel (+K3)" if seqprod
+                       else "ring_kl_kernel (K2kl, incl. its K3 finalize launch)" if kl
                        else "ring_lag_kernel (K2, incl. its K3 finalize launch)"),
             "algorithmic_bytes_per_token": bytes_tok, "tokens_per_launch": launch_tokens,
             "kernel_ms_per_step": round(kern_ms, 3)}
@@ -432,7 +448,7 @@ def impl_ours(args, wl, variant):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl.description, "variant": variant, "aggregation": args.aggregation,
-                       "vocab": wl.vocab,
+                       "kl_weight": args.kl_weight, "vocab": wl.vocab,
                        "prompts_per_gpu": args.prompts or wl.prompts, "group": wl.group, "max_len": wl.max_len,
                        "async_ratio": wl.alpha, "tokens_per_gpu": dw.T, "tokens_global": tokens_global,
                        "chunk_tokens": chunk, "logits_pool_rows": dw.pool_rows,
@@ -458,7 +474,7 @@ def main():
     from paper_2510_11345_b200 import synth as S
 
     wl = S.WORKLOADS[args.workload]
-    variant = args.variant or wl.variant
+    variant = args.variant or ("grpo" if args.kl_weight > 0 else wl.variant)
     if args.impl == "reference":
         impl_reference(args, wl, variant)
     else:

@@ -24,7 +24,7 @@ bool is_aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p
 
 struct RingGeometry {
     bool ok = false;
-    int kind = 2;  // 0 small, 1 large, 2 lag
+    int kind = 2;  // 0 small, 1 large, 2 lag, 3 lag + exact-KL reference row
     int cs = 1, ncw = 0, nvt = 0;
     int row_vecs = 0, slice_vecs = 0, nchunks = 0, nslots = 0;
     size_t smem = 0;
@@ -119,6 +119,48 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
     return g;
 }
 
+// Exact-KL lag kernel: bf16 policy and reference rows (both 16-byte aligned rows),
+// the smallest cluster whose slice fits 12 warps x NVT vectors of each row; every
+// ring slot holds a chunk of both rows.
+RingGeometry ring_geometry_kl(const rf_batch* b, const rf_outputs* o) {
+    RingGeometry g;
+    g.kind = 3;
+    if (b->logits_dtype != RF_DTYPE_BF16 || !b->ref_logits) return g;
+    g.row_vecs = (b->vocab + 7) / 8;
+    if (!is_aligned(b->logits, 16) || (b->logits_row_stride * 2) % 16 != 0) return g;
+    if (!is_aligned(b->ref_logits, 16) || (b->ref_row_stride * 2) % 16 != 0) return g;
+    if (b->logits_row_stride < static_cast<int64_t>(g.row_vecs) * 8) return g;
+    if (b->ref_row_stride < static_cast<int64_t>(g.row_vecs) * 8) return g;
+    const size_t os = dtype_size(o->dlogits_dtype);
+    if (o->dlogits == nullptr || !is_aligned(o->dlogits, 16)) return g;
+    if ((o->dlogits_row_stride * static_cast<int64_t>(os)) % 16 != 0) return g;
+    if (o->dlogits_row_stride < static_cast<int64_t>(g.row_vecs) * 8) return g;
+    const int ncw = rf::kRingWarpsLag, nct = ncw * 32;
+    const size_t tail = rf::kRingKLTailBytes + rf::kRingLagBarrierBytes;
+    for (int cs = 1; cs <= 8; cs *= 2) {
+        const int slice = (g.row_vecs + cs - 1) / cs;
+        if (cs > 1 && slice * (cs - 1) >= g.row_vecs) break;
+        int nvt = 0;
+        for (int q : rf::kRingNvtKL)
+            if (static_cast<int64_t>(q) * nct >= slice) {
+                nvt = q;
+                break;
+            }
+        if (!nvt) continue;
+        const size_t cb = static_cast<size_t>(nct) * rf::lag_vpc(nvt) * 16;
+        g.cs = cs;
+        g.ncw = ncw;
+        g.nvt = nvt;
+        g.slice_vecs = slice;
+        g.nchunks = static_cast<int>((slice + cb / 16 - 1) / (cb / 16));
+        g.nslots = static_cast<int>((static_cast<size_t>(max_optin_smem()) - tail) / (2 * cb + 16));
+        g.smem = static_cast<size_t>(g.nslots) * (2 * cb + 16) + tail;
+        g.ok = g.nslots >= 2;
+        return g;
+    }
+    return g;
+}
+
 int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t smem) {
     struct Key {
         bool ib, ob;
@@ -134,7 +176,8 @@ int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t s
             k.smem == smem)
             return k.val;
     int n = 0;
-    const cudaError_t e = kind == 2 ? rf::ring_lag_max_clusters(ib, ob, ncw, nvt, cs, smem, &n)
+    const cudaError_t e = kind == 3 ? rf::ring_kl_max_clusters(ob, nvt, cs, smem, &n)
+                          : kind == 2 ? rf::ring_lag_max_clusters(ib, ob, ncw, nvt, cs, smem, &n)
                                     : rf::ring_max_clusters(ib, ob, ncw, nvt, cs, smem, &n);
     if (e != cudaSuccess || n <= 0) {
         cudaGetLastError();
@@ -437,7 +480,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
         }
     } else {
         RingGeometry g;
-        if (kernel != RF_KERNEL_GENERIC && !needs_ref) g = ring_geometry(b, o);
+        if (kernel != RF_KERNEL_GENERIC) g = needs_ref ? ring_geometry_kl(b, o) : ring_geometry(b, o);
         if (kernel == RF_KERNEL_RING && !g.ok) return RF_ERR_UNSUPPORTED_LAYOUT;
         if (g.ok) {
             p.slice_vecs = g.slice_vecs;
@@ -446,10 +489,11 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.nslots = g.nslots;
             const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
             const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-            const cudaError_t e = g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s)
-                                              : rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
+            const cudaError_t e = g.kind == 3   ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
+                                  : g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s)
+                                                : rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
             if (e != cudaSuccess) return RF_ERR_CUDA;
-            nparts = g.kind == 2 ? 2 * ncl : ncl;  // lag kernel: one partial row per scalar warp
+            nparts = g.kind >= 2 ? 2 * ncl : ncl;  // lag kernels: one partial row per scalar warp
         } else {
             const int grid = generic_grid(b->num_tokens);
             if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;

@@ -47,6 +47,13 @@ __host__ __device__ constexpr int lag_vpc(int nvt) { return (RF_LAG_VPC > 0 && n
 constexpr size_t kRingLagTailBytes = 1088;  // exchange / reduce / broadcast words + 4 exchange mbarriers
 constexpr size_t kRingLagBarrierBytes = 48;
 
+// Exact-KL lag kernel (rf_ring_kl.cu): policy and reference rows co-resident,
+// 12 consumer warps, bf16 logits; NVT = 13 covers a quarter Qwen3 row (4-CTA cluster).
+constexpr int kRingNvtKL[2] = {4, 13};
+constexpr size_t kRingKLTailBytes = 2176;  // [4][8] 40-byte exchange slots + 5 x [2][NCW] partials + broadcast
+cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int nclusters, size_t smem,
+                           cudaStream_t st);
+cudaError_t ring_kl_max_clusters(bool out_bf16, int nvt, int cs, size_t smem, int* out);
 cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
                             size_t smem, cudaStream_t st);
 cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);

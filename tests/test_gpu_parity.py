@@ -114,6 +114,30 @@ def test_grpo_kl_token_mean_mapping_a():
     compare(case, cfg, gpu, ref)
 
 
+@pytest.mark.parametrize("V", [1003, 4099, 32000, 151936])
+@pytest.mark.parametrize("kernel", ["ring", "generic"])
+def test_grpo_kl_fast_path(V, kernel):
+    """Exact-KL GRPO on the lag kernel (policy + reference rows co-resident; the
+    Qwen3 row spans a 4-CTA cluster) against the oracle, and the generic kernel."""
+    case = make_case(21, T_seqs=6 if V > 100000 else 12, G=3, V=V, max_len=6, mapping="A", stale=0.2, kl=True)
+    cfg = _cfg("grpo", kl_weight=0.1)
+    pb = to_device_batch(case, with_ref=True, normalization=L.Normalization.global_token)
+    gpu = rf.loss_and_grad(cfg, pb, kernel=kernel)
+    ref = run_oracle(case, cfg, normalization=1)
+    compare(case, cfg, gpu, ref)
+
+
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
+def test_grpo_kl_fast_path_mapping_b(out):
+    """Rows shared per sequence (KL per trajectory through the 1/(N·L_i) scale)."""
+    case = make_case(22, T_seqs=12, G=4, V=32000, max_len=9, mapping="B", stale=0.3, kl=True)
+    cfg = _cfg("grpo", kl_weight=0.25)
+    pb = to_device_batch(case, with_ref=True)
+    gpu = rf.loss_and_grad(cfg, pb, dlogits_dtype=out, kernel="ring")
+    ref = run_oracle(case, cfg, normalization=0)
+    compare(case, cfg, gpu, ref, out_dtype=out)
+
+
 def test_f32_logp_inputs_and_grad_sign():
     case = make_case(19, T_seqs=8, G=4, V=32000, max_len=8, mapping="A", stale=0.2)
     cfg = _cfg("ppo")
