@@ -137,12 +137,15 @@ RingGeometry ring_geometry_kl(const rf_batch* b, const rf_outputs* o) {
     if (o->dlogits_row_stride < static_cast<int64_t>(g.row_vecs) * 8) return g;
     const int ncw = rf::kRingWarpsLag, nct = ncw * 32;
     const size_t tail = rf::kRingKLTailBytes + rf::kRingLagBarrierBytes;
-    for (int cs = 1; cs <= 8; cs *= 2) {
+    // RF_KL_NVT caps the vectors per thread (A/B knob: 13 -> 4-CTA clusters at Qwen3)
+    int nvt_cap = rf::kRingNvtKL[2];
+    if (const char* e = std::getenv("RF_KL_NVT")) nvt_cap = std::atoi(e);
+    for (int cs = 1; cs <= 8; ++cs) {  // any cluster size: the slice must fit the registers
         const int slice = (g.row_vecs + cs - 1) / cs;
         if (cs > 1 && slice * (cs - 1) >= g.row_vecs) break;
         int nvt = 0;
         for (int q : rf::kRingNvtKL)
-            if (static_cast<int64_t>(q) * nct >= slice) {
+            if (q <= nvt_cap && static_cast<int64_t>(q) * nct >= slice) {
                 nvt = q;
                 break;
             }

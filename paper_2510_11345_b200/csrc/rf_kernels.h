@@ -49,7 +49,7 @@ constexpr size_t kRingLagBarrierBytes = 48;
 
 // Exact-KL lag kernel (rf_ring_kl.cu): policy and reference rows co-resident,
 // 12 consumer warps, bf16 logits; NVT = 13 covers a quarter Qwen3 row (4-CTA cluster).
-constexpr int kRingNvtKL[2] = {4, 13};
+constexpr int kRingNvtKL[3] = {4, 10, 13};  // 13: 4-CTA clusters at V=151,936 (5-CTA with RF_KL_NVT=10: -6%)
 constexpr size_t kRingKLTailBytes = 2176;  // [4][8] 40-byte exchange slots + 5 x [2][NCW] partials + broadcast
 cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int nclusters, size_t smem,
                            cudaStream_t st);

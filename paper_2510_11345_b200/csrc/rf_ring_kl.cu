@@ -583,11 +583,13 @@ cudaError_t kl_dispatch(const KParams& p, bool ob, int nvt, int cs, int ncl, siz
         switch (nvt) {
             case kRingNvtKL[0]: return launch_kl_t<true, kRingWarpsLag, kRingNvtKL[0]>(p, cs, ncl, smem, st, maxc);
             case kRingNvtKL[1]: return launch_kl_t<true, kRingWarpsLag, kRingNvtKL[1]>(p, cs, ncl, smem, st, maxc);
+            case kRingNvtKL[2]: return launch_kl_t<true, kRingWarpsLag, kRingNvtKL[2]>(p, cs, ncl, smem, st, maxc);
         }
     } else {
         switch (nvt) {
             case kRingNvtKL[0]: return launch_kl_t<false, kRingWarpsLag, kRingNvtKL[0]>(p, cs, ncl, smem, st, maxc);
             case kRingNvtKL[1]: return launch_kl_t<false, kRingWarpsLag, kRingNvtKL[1]>(p, cs, ncl, smem, st, maxc);
+            case kRingNvtKL[2]: return launch_kl_t<false, kRingWarpsLag, kRingNvtKL[2]>(p, cs, ncl, smem, st, maxc);
         }
     }
     return cudaErrorInvalidValue;
