@@ -214,6 +214,10 @@ __device__ __forceinline__ void st_async_f32(uint32_t cluster_addr, float v, uin
 __device__ __forceinline__ void st_release_cluster_u32(uint32_t cluster_addr, uint32_t v) {
     asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");

@@ -269,6 +269,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 if (csize > 1) {
                     const uint32_t xs = row_iter & 3;
                     XSlot* mine = &xslot[xs * 8 + rank];
+                    // payload to every peer, one cluster fence, then the sequence words
+                    // (one fence instead of a release per peer)
                     for (uint32_t q = 0; q < csize; ++q) {
                         if (q == rank) continue;
                         st_cluster_f64(mapa(smem_u32(&mine->S), q), Sw);
@@ -276,8 +278,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                         st_cluster_f64(mapa(smem_u32(&mine->Sy), q), Syw);
                         st_cluster_f32(mapa(smem_u32(&mine->M), q), Mw);
                         st_cluster_f32(mapa(smem_u32(&mine->My), q), Myw);
-                        st_release_cluster_u32(mapa(smem_u32(&mine->seq), q), row_iter + 1);
                     }
+                    fence_acq_rel_cluster();
+                    for (uint32_t q = 0; q < csize; ++q)
+                        if (q != rank) st_relaxed_cluster_u32(mapa(smem_u32(&mine->seq), q), row_iter + 1);
                     for (uint32_t q = 0; q < csize; ++q) {
                         if (q == rank) continue;
                         const uint32_t a = smem_u32(&xslot[xs * 8 + q].seq);
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 bc->B = static_cast<float>(kc);
                 bc->lseL = lseL;
                 if (tok_ok) {
-                    const double pt = exp(lp);
+                    const double pt = tr.ratio * pre.eb;  // exp(lp) = ratio · exp(b)
                     const double dt = static_cast<double>(x_tok) - static_cast<double>(y_tok);
                     bc->tok_val = (tr.k - tr.k * pt) + kc * pt * (dt - D);
                     bc->tok = tok;
