@@ -74,6 +74,11 @@ __device__ __forceinline__ double combine_factor(float m, float mx) {
 #ifndef RF_XCHG_SPIN
 #define RF_XCHG_SPIN 0  // exchange wait: 1 = try_wait polling with a 32 ns back-off
 #endif
+// Scalar lane fences its previous row's global output stores before waiting for the
+// next partials, so the exchange's release fence finds nothing outstanding (A/B knob).
+#ifndef RF_PREFENCE
+#define RF_PREFENCE 0
+#endif
 // Write phase: straight-line stores for chunks with no padded / missing vectors.
 #ifndef RF_WRITE_FAST
 #define RF_WRITE_FAST 1  // A/B on B200: +6% (per-vector branches serialised the store math)

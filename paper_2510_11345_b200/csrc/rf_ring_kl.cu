@@ -247,6 +247,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 const TokenPre pre = token_pre(p, t, seq);
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
+                if (RF_PREFENCE) fence_acq_rel_cluster();  // drain this lane's output stores while idle
                 support_wait(bar_red + 8 * par, ph, 128);
                 // CTA partials, warp order
                 float Mw = -CUDART_INF_F, Myw = -CUDART_INF_F;

@@ -188,6 +188,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                if (RF_PREFENCE) fence_acq_rel_cluster();  // drain this lane's output stores while idle
                 support_wait(bar_red + 8 * par, ph, 128);
                 if (kPhaseCounters && p.dbg) pc.lap(d_red);
                 float Mw;
