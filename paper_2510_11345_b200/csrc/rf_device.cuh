@@ -217,6 +217,14 @@ __device__ __forceinline__ void st_release_cluster_u32(uint32_t cluster_addr, ui
 __device__ __forceinline__ void st_relaxed_cluster_u32(uint32_t cluster_addr, uint32_t v) {
     asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_cluster_u64(uint32_t cluster_addr, uint64_t v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.u64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_cluster_u64(uint32_t addr) {
+    uint64_t v;
+    asm volatile("ld.relaxed.cluster.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    return v;
+}
 __device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
     uint32_t v;

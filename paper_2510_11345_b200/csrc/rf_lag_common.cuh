@@ -71,6 +71,9 @@ __device__ __forceinline__ double combine_factor(float m, float mx) {
 #ifndef RF_XCHG_MBAR
 #define RF_XCHG_MBAR 0
 #endif
+#ifndef RF_XCHG_TAG
+#define RF_XCHG_TAG 0  // 1: fence-free tagged 64-bit words (see rf_ring_lag.cu)
+#endif
 #ifndef RF_XCHG_SPIN
 #define RF_XCHG_SPIN 0  // exchange wait: 1 = try_wait polling with a 32 ns back-off
 #endif

@@ -93,7 +93,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             mbar_init(bar_red + 8 * q, NCW);  // one arrival per consumer warp partial
             mbar_init(bar_bc + 8 * q, 1);
         }
-        for (int q = 0; q < 32; ++q) xslot[q].seq = 0u;
+        for (int q = 0; q < 32; ++q) {
+            xslot[q].S = 0.0;  // tag 0 in both words: never a live use
+            xslot[q].seq = 0u;
+        }
         for (int q = 0; q < 4; ++q) mbar_init(xbar + 8 * q, 1);  // the local scalar's arrive.expect_tx
         fence_mbar_init();
     }
@@ -238,6 +241,30 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                             mbar_wait_backoff(xbar + 8 * xs, (row_iter >> 2) & 1, 32);
                         else
                             support_wait(xbar + 8 * xs, (row_iter >> 2) & 1, 32);
+                        if (kPhaseCounters && p.dbg) pc.lap(d_x);
+                    } else if (RF_XCHG_TAG) {
+                        // fence-free: two single-copy-atomic 64-bit words per peer, each
+                        // carrying the slot's use tag — (S with the tag in its 8 low mantissa
+                        // bits, 2^-44 relative) and (M, tag) — polled until both match
+                        const uint32_t xs = row_iter & 3;
+                        const uint32_t tag = (row_iter >> 2) + 1;
+                        const uint64_t w0 =
+                            (static_cast<uint64_t>(__double_as_longlong(Sw)) & ~0xffull) | (tag & 0xffu);
+                        const uint64_t w1 = static_cast<uint64_t>(__float_as_uint(Mw)) | (static_cast<uint64_t>(tag) << 32);
+                        XSlot* mine = &xslot[xs * 8 + rank];
+                        for (uint32_t q = 0; q < csize; ++q) {
+                            if (q == rank) continue;
+                            st_relaxed_cluster_u64(mapa(smem_u32(&mine->S), q), w0);
+                            st_relaxed_cluster_u64(mapa(smem_u32(&mine->M), q), w1);
+                        }
+                        if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                        for (uint32_t q = 0; q < csize; ++q) {
+                            if (q == rank) continue;
+                            const uint32_t a0 = smem_u32(&xslot[xs * 8 + q].S), a1 = smem_u32(&xslot[xs * 8 + q].M);
+                            while ((ld_relaxed_cluster_u64(a1) >> 32) != tag ||
+                                   (ld_relaxed_cluster_u64(a0) & 0xffu) != (tag & 0xffu))
+                                __nanosleep(32);
+                        }
                         if (kPhaseCounters && p.dbg) pc.lap(d_x);
                     } else {
                         const uint32_t slot = (row_iter & 3) * 8 + rank;
