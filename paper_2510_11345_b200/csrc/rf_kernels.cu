@@ -261,34 +261,49 @@ __global__ void __launch_bounds__(NT) generic_kernel(const __grid_constant__ KPa
 // ===========================================================================
 __global__ void seq_kernel(const __grid_constant__ KParams p, int64_t seq_begin, int64_t nseq,
                            double* __restrict__ coef_out) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= nseq) return;
+    // One warp per sequence.  The trajectory sums keep the reference's token order
+    // (lanes load 32 tokens at a time, every lane adds them in order from shuffles,
+    // so every lane holds the exact sequential sums); the per-token outputs are
+    // written by all lanes in parallel.
+    const int lane = threadIdx.x & 31;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= nseq) return;  // whole warps
     const int64_t s = seq_begin + i;
     const int64_t t_base = p.seq_offsets[0];  // tokens of this call start at seq_offsets[0]
     const int64_t t0 = p.seq_offsets[s] - t_base, t1 = p.seq_offsets[s + 1] - t_base;
     const int64_t len = t1 - t0;
     const bool kl = (p.variant == RF_GRPO) && (p.kl_weight > 0.0);
+    const bool dppo = p.variant == RF_DECOUPLED_PPO;
+    const bool cap = p.mismatch_cap > 0.0;
     double LR = 0.0, logp_sum = 0.0, LPX = 0.0, LM = 0.0;
-    for (int64_t t = t0; t < t1; ++t) {
-        const double lp = p.token_logp[t];
-        const double b = load_logp(p.behavior_logp, t, p.logp_f64);
-        LR = __dadd_rn(LR, __dsub_rn(lp, b));
-        logp_sum = __dadd_rn(logp_sum, lp);
-        if (p.variant == RF_DECOUPLED_PPO) LPX = __dadd_rn(LPX, __dsub_rn(lp, load_logp(p.prox_logp, t, p.logp_f64)));
-        if (p.mismatch_cap > 0.0) LM = __dadd_rn(LM, __dsub_rn(b, load_logp(p.engine_logp, t, p.logp_f64)));
+    for (int64_t tb = t0; tb < t1; tb += 32) {
+        const int64_t t = tb + lane;
+        const bool ok = t < t1;
+        const double lp = ok ? p.token_logp[t] : 0.0;
+        const double b = ok ? load_logp(p.behavior_logp, t, p.logp_f64) : 0.0;
+        const double dlr = __dsub_rn(lp, b);
+        const double dpx = (dppo && ok) ? __dsub_rn(lp, load_logp(p.prox_logp, t, p.logp_f64)) : 0.0;
+        const double dm = (cap && ok) ? __dsub_rn(b, load_logp(p.engine_logp, t, p.logp_f64)) : 0.0;
+        const int n = static_cast<int>((t1 - tb) < 32 ? (t1 - tb) : 32);
+        for (int k = 0; k < n; ++k) {  // token order (losses.cpp:187-252)
+            LR = __dadd_rn(LR, __shfl_sync(0xffffffffu, dlr, k));
+            logp_sum = __dadd_rn(logp_sum, __shfl_sync(0xffffffffu, lp, k));
+            if (dppo) LPX = __dadd_rn(LPX, __shfl_sync(0xffffffffu, dpx, k));
+            if (cap) LM = __dadd_rn(LM, __shfl_sync(0xffffffffu, dm, k));
+        }
     }
     uint32_t flags = 0;
     const double em = exp(LM);
-    const double m = p.mismatch_cap > 0.0 ? ((p.mismatch_cap < em) ? p.mismatch_cap : em) : 1.0;
-    if (p.mismatch_cap > 0.0 && em > p.mismatch_cap) flags |= RF_FLAG_MISMATCH_CAPPED;
+    const double m = cap ? ((p.mismatch_cap < em) ? p.mismatch_cap : em) : 1.0;
+    if (cap && em > p.mismatch_cap) flags |= RF_FLAG_MISMATCH_CAPPED;
     const double r = exp(LR);
     if (!isfinite(r)) {
         flags |= RF_FLAG_NONFINITE;
-        atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
+        if (lane == 0) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
     }
     const double A = p.advantages[s];
     double po = 0.0, tp = 0.0;
-    if (p.variant == RF_DECOUPLED_PPO) {
+    if (dppo) {
         po = exp(__dsub_rn(LR, LPX));
         tp = exp(LPX);
     }
@@ -300,27 +315,37 @@ __global__ void seq_kernel(const __grid_constant__ KParams p, int64_t seq_begin,
     if (k == 0.0) flags |= RF_FLAG_ZERO_COEF;
     const double contrib = __dmul_rn(sm, value);
     const double ks = p.normalization == RF_NORM_GLOBAL_TOKEN ? p.inv_t : p.inv_n / static_cast<double>(len);
-    Partials part;
-    part.zero();
-    for (int64_t t = t0; t < t1; ++t) {
-        TokenResult tr;
-        tr.k = k;
-        tr.flags = flags;
-        tr.ratio = exp(p.token_logp[t] - load_logp(p.behavior_logp, t, p.logp_f64));
-        tr.loss = (t == t0) ? contrib : 0.0;
-        double kl_scaled = 0.0;
+    double loss_sum = 0.0, kl_sum = 0.0;
+    for (int64_t t = t0 + lane; t < t1; t += 32) {
+        double loss = (t == t0) ? contrib : 0.0;
         if (kl) {
             const double klv = p.tok_klx[t];
-            kl_scaled = __dmul_rn(ks, klv);
-            tr.loss -= __dmul_rn(__dmul_rn(ks, p.kl_weight), klv);
+            kl_sum += __dmul_rn(ks, klv);
+            loss -= __dmul_rn(__dmul_rn(ks, p.kl_weight), klv);
         }
         coef_out[t] = k;
-        if (p.token_ratio) p.token_ratio[t] = tr.ratio;
-        if (p.token_loss) p.token_loss[t] = tr.loss;
+        if (p.token_ratio) p.token_ratio[t] = exp(p.token_logp[t] - load_logp(p.behavior_logp, t, p.logp_f64));
+        if (p.token_loss) p.token_loss[t] = loss;
         if (p.token_flags) p.token_flags[t] = static_cast<uint8_t>(flags);
-        part.add_token(tr, kl_scaled);
+        loss_sum += loss;
     }
-    part.store(p.partials + static_cast<size_t>(i) * RF_NUM_SCALARS);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // fixed tree: deterministic
+        loss_sum += __shfl_xor_sync(0xffffffffu, loss_sum, o);
+        kl_sum += __shfl_xor_sync(0xffffffffu, kl_sum, o);
+    }
+    if (lane == 0) {
+        const double n = static_cast<double>(len);
+        double* dst = p.partials + static_cast<size_t>(i) * RF_NUM_SCALARS;
+        dst[RF_SCALAR_LOSS] = loss_sum;
+        dst[RF_SCALAR_TOKENS] = n;
+        dst[RF_SCALAR_CLIPPED] = (flags & RF_FLAG_CLIPPED) ? n : 0.0;
+        dst[RF_SCALAR_NONFINITE] = (flags & RF_FLAG_NONFINITE) ? n : 0.0;
+        dst[RF_SCALAR_ZERO_COEF] = (flags & RF_FLAG_ZERO_COEF) ? n : 0.0;
+        dst[RF_SCALAR_MISMATCH] = (flags & RF_FLAG_MISMATCH_CAPPED) ? n : 0.0;
+        dst[RF_SCALAR_KL] = kl_sum;
+        dst[RF_SCALAR_COEF_ABS] = fabs(k) * n;
+    }
 }
 
 // ===========================================================================
@@ -351,8 +376,8 @@ cudaError_t launch_generic(const KParams& p, bool in_bf16, bool out_bf16, int gr
 }
 
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st) {
-    const int nt = 128;
-    const int grid = static_cast<int>((nseq + nt - 1) / nt);
+    const int nt = 128;  // four sequences (one per warp) per block
+    const int grid = static_cast<int>((nseq + 3) / 4);
     seq_kernel<<<grid, nt, 0, st>>>(p, seq_begin, nseq, coef);
     return cudaGetLastError();
 }
