@@ -125,6 +125,19 @@ __device__ __forceinline__ uint64_t vec_exp(uint4& v, uint64_t L2, uint64_t negC
     }
 }
 
+// f16x2 e vector -> bf16x2 e·f (the staged dlogits vector of the TMA-store path)
+__device__ __forceinline__ uint4 vec_out_bf16(const uint4& e, uint64_t f2) {
+    const uint32_t w[4] = {e.x, e.y, e.z, e.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float2 h = unpack_f16x2(w[q]);
+        const uint64_t m = fmul2(pk2(h.x, h.y), f2);
+        o[q] = pack_bf16x2(lo2(m), hi2(m));
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 template <bool OUT_BF16, int EPV>
 __device__ __forceinline__ void store_vec(uint8_t* dst, const uint4& e, uint64_t f2, bool in_bf16) {
     if (in_bf16) {
