@@ -26,7 +26,7 @@ struct RingGeometry {
     bool ok = false;
     int kind = 2;  // 0 small, 1 large, 2 lag, 3 lag + exact-KL reference row
     int cs = 1, ncw = 0, nvt = 0;
-    int row_vecs = 0, slice_vecs = 0, nchunks = 0, nslots = 0, nwslots = 0;
+    int row_vecs = 0, slice_vecs = 0, nchunks = 0, nslots = 0;
     size_t smem = 0;
 };
 
@@ -110,16 +110,9 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
         g.nvt = nvt;
         g.slice_vecs = slice;
         g.nchunks = static_cast<int>((slice + cb / 16 - 1) / (cb / 16));
-        // [nslots x (chunk + full/empty barriers)] + row barriers + tail words; the lag
-        // kernel's TMA-store path (RF_LAG_STAGE=1, bf16 -> bf16) takes kLagStageSlots
-        // of those slots as its dlogits staging ring
-        const int total = static_cast<int>((static_cast<size_t>(smem_cap) - tail) / (cb + 16));
-        const char* stage = std::getenv("RF_LAG_STAGE");
-        const bool staged = g.kind == 2 && stage && stage[0] == '1' && b->logits_dtype == RF_DTYPE_BF16 &&
-                            o->dlogits_dtype == RF_DTYPE_BF16;
-        g.nwslots = staged ? rf::kLagStageSlots : 0;
-        g.nslots = total - g.nwslots;
-        g.smem = static_cast<size_t>(total) * (cb + 16) + tail;
+        // [nslots x (chunk + full/empty barriers)] + row barriers + tail words
+        g.nslots = static_cast<int>((static_cast<size_t>(smem_cap) - tail) / (cb + 16));
+        g.smem = static_cast<size_t>(g.nslots) * (cb + 16) + tail;
         g.ok = g.nslots >= 2;
         return g;
     }
@@ -465,7 +458,6 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.row_vecs = g.row_vecs;
             p.nchunks = g.nchunks;
             p.nslots = g.nslots;
-            p.nwslots = g.nwslots;
             const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
             const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
             if (rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s) != cudaSuccess)
@@ -498,7 +490,6 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.row_vecs = g.row_vecs;
             p.nchunks = g.nchunks;
             p.nslots = g.nslots;
-            p.nwslots = g.nwslots;
             const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
             const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
             const cudaError_t e = g.kind == 3   ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)

@@ -57,7 +57,6 @@ struct KParams {
     int32_t row_vecs;     // 16-byte vectors per row (padded)
     int32_t nchunks;      // chunks per slice
     int32_t nslots;       // ring slots
-    int32_t nwslots;      // lag kernel: dlogits staging slots drained by TMA bulk stores (0 = direct stores)
     int32_t mode;         // 0 = fused loss+dlogits, 1 = stats only (lse/lp), 2 = write with known lse/coef
     unsigned long long* dbg;  // optional per-phase cycle counters (RF_DEBUG_COUNTERS), else nullptr
 };

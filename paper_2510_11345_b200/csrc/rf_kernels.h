@@ -44,11 +44,6 @@ __host__ __device__ constexpr unsigned lag_tmem_cols(int ncw) { return (512u / (
 #define RF_LAG_VPC 5  // 30 KB chunks at 12 consumer warps: measured best of {2,3,4,5,7,9,13}
 #endif
 __host__ __device__ constexpr int lag_vpc(int nvt) { return (RF_LAG_VPC > 0 && nvt >= 9) ? RF_LAG_VPC : ring_vpc(nvt); }
-// dlogits staging slots of the lag kernel's TMA-store path (RF_LAG_STAGE=1 at run time)
-#ifndef RF_LAG_WSLOTS
-#define RF_LAG_WSLOTS 3
-#endif
-constexpr int kLagStageSlots = RF_LAG_WSLOTS;
 constexpr size_t kRingLagTailBytes = 1088;  // exchange / reduce / broadcast words + 4 exchange mbarriers
 constexpr size_t kRingLagBarrierBytes = 48;
 

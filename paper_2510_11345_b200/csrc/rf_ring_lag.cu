@@ -44,24 +44,16 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
     constexpr uint32_t TCOLS = lag_tmem_cols(NCW);  // TMEM columns per consumer warp
     static_assert(NVT * 4 <= static_cast<int>(TCOLS), "a thread's e values must fit its TMEM columns");
     constexpr int REGS_C = lag_regs_consumer(NCW);
-    constexpr uint32_t kStageSlots = static_cast<uint32_t>(kLagStageSlots);
 
-    // smem: [nslots read chunks][nws staging chunks][full][empty][sfull][sfree][x(2)][red(2)][bc(2)] + tail
+    // smem: [nslots chunks][full][empty][x(2)][red(2)][bc(2)] + tail
     extern __shared__ __align__(1024) uint8_t smem[];
     const int nslots = p.nslots;
-    // dlogits staging ring drained by TMA bulk stores (bf16 -> bf16, fused pass only)
-    constexpr bool kStageOK = IN_BF16 && OUT_BF16;
-    const int nws = (kStageOK && p.mode == 0) ? p.nwslots : 0;
-    const int nws_alloc = p.nwslots;
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t stg_base = sbase + nslots * CHUNK_BYTES;
-    const uint32_t bar_full = sbase + (nslots + nws_alloc) * CHUNK_BYTES;
+    const uint32_t bar_full = sbase + nslots * CHUNK_BYTES;
     const uint32_t bar_empty = bar_full + nslots * 8;
-    const uint32_t sbar_full = bar_empty + nslots * 8;    // [nws] 12 consumer warps staged the chunk
-    const uint32_t sbar_free = sbar_full + nws_alloc * 8;  // [nws] the TMA store has read the chunk
-    const uint32_t bar_red = sbar_free + nws_alloc * 8 + 16;  // [2] consumers -> scalar: CTA partial (row parity)
+    const uint32_t bar_red = bar_empty + nslots * 8 + 16;  // [2] consumers -> scalar: CTA partial (row parity)
     const uint32_t bar_bc = bar_red + 16;            // [2] scalar -> consumers: coefficient (row parity)
-    uint8_t* tail = smem + (nslots + nws_alloc) * CHUNK_BYTES + (nslots + nws_alloc) * 16 + 48;
+    uint8_t* tail = smem + nslots * CHUNK_BYTES + nslots * 16 + 48;
     // Cluster exchange slots [row % 4][sender rank]: written remotely by the peer's
     // scalar warp, guarded by a sequence word (row + 1) instead of an mbarrier phase,
     // so a peer running ahead can never alias a phase (a peer is at most one row of
@@ -100,10 +92,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         for (int q = 0; q < 2; ++q) {
             mbar_init(bar_red + 8 * q, NCW);  // one arrival per consumer warp partial
             mbar_init(bar_bc + 8 * q, 1);
-        }
-        for (int q = 0; q < nws_alloc; ++q) {
-            mbar_init(sbar_full + 8 * q, NCW);
-            mbar_init(sbar_free + 8 * q, 1);
         }
         for (int q = 0; q < 32; ++q) {
             xslot[q].S = 0.0;  // tag 0 in both words: never a live use
@@ -171,35 +159,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 atomicAdd(p.dbg + 10, dw);
                 atomicAdd(p.dbg + 11, dt);
             }
-        }
-        __syncwarp();
-    } else if (warp == NCW + 3) {
-        // ----------------------- TMA store warp (staging ring) -----------------------
-        if (nws > 0 && lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
-            uint32_t k = 0;  // staged chunks so far (slot k % nws, use k / nws)
-            for (int64_t t = cid; t < p.T; t += ncl) {
-                uint8_t* drow = reinterpret_cast<uint8_t*>(p.dlogits) + static_cast<size_t>(t) * p.dl_stride * 2 +
-                                static_cast<size_t>(slice_begin) * 16;
-                for (int c = 0; c < nchunks; ++c, ++k) {
-                    const uint32_t ws = k % kStageSlots;
-                    mbar_wait_sleep(sbar_full + 8 * ws, (k / kStageSlots) & 1);
-                    const int v0 = c * CHUNK_VECS;
-                    int nv = min(CHUNK_VECS, slice_len - v0);
-                    // the row's padded tail vector is stored element-wise by its owner thread
-                    if (has_tail && tail_vec - slice_begin >= v0 && tail_vec - slice_begin < v0 + nv) nv -= 1;
-                    if (nv > 0)
-                        bulk_s2g(drow + static_cast<size_t>(v0) * 16, stg_base + ws * CHUNK_BYTES,
-                                 static_cast<uint32_t>(nv) * 16, pol);
-                    bulk_commit();
-                    // free the oldest slot still being read once only nws-1 groups are in flight
-                    if (k + 1 >= kStageSlots) {
-                        bulk_wait_read<kLagStageSlots - 1>();
-                        mbar_arrive(sbar_free + 8 * ((k + 1 - kStageSlots) % kStageSlots));
-                    }
-                }
-            }
-            bulk_wait_all();
         }
         __syncwarp();
     } else if (warp == NCW + 1 || warp == NCW + 2) {
@@ -422,7 +381,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         pcc.start();
         const long long t_begin = pcc.t;
         const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
-        uint32_t wk = 0;  // staged dlogits chunks so far (TMA-store path)
 
         // copy-in + max + exp sweep + CTA reduction of row t into r[]; returns C_t.
         auto stream_row = [&](uint32_t row_iter, bool park_prev) -> float {
@@ -539,57 +497,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             const uint64_t f2 = pk2(f, f);
             uint8_t* drow = reinterpret_cast<uint8_t*>(p.dlogits) + static_cast<size_t>(t) * p.dl_stride * OES;
             uint8_t* dthr = drow + thr_off;
-            if (kStageOK && nws > 0) {
-                // Staged: bf16 vectors into the staging slot (the slice order of the chunk),
-                // then the store warp drains the chunk with one TMA bulk store while the
-                // consumers stream the next row.  The padded tail vector goes out directly.
-                const int sv_tok = tokv >= 0 ? tokv / EPV - slice_begin : -1;
-#pragma unroll 1
-                for (int c = 0; c < nchunks; ++c, ++wk) {
-                    uint4 e[VPC];
-                    if (c * VPC + VPC <= NVT) {
-                        tmem_ld_vecs<VPC>(tm + 4 * (c * VPC), e);
-                    } else {
-#pragma unroll
-                        for (int h = 0; h < VPC; ++h)
-                            if (c * VPC + h < NVT) tmem_ld4(tm + 4 * (c * VPC + h), e[h]);
-                    }
-                    const uint32_t ws = wk % kStageSlots;
-                    if (wk >= kStageSlots) cons_wait(sbar_free + 8 * ws, ((wk / kStageSlots) - 1) & 1);
-                    const uint32_t slot = stg_base + ws * CHUNK_BYTES;
-                    if (c * VPC + VPC <= jfull) {
-#pragma unroll
-                        for (int h = 0; h < VPC; ++h) sts128_raw(slot + (h * NCT + tid) * 16, vec_out_bf16(e[h], f2));
-                    } else {
-#pragma unroll
-                        for (int h = 0; h < VPC; ++h) {
-                            const int jj = c * VPC + h;
-                            if (jj < jmax) {
-                                if (jj != tail_j)
-                                    sts128_raw(slot + (h * NCT + tid) * 16, vec_out_bf16(e[h], f2));
-                                else
-                                    store_vec_partial<OUT_BF16, EPV>(dthr + static_cast<size_t>(c) * CHUNK_VECS * EPV * OES +
-                                                                         static_cast<size_t>(h) * NCT * EPV * OES,
-                                                                     e[h], f, IN_BF16, tail_valid);
-                            }
-                        }
-                    }
-                    if (sv_tok >= c * CHUNK_VECS && sv_tok < (c + 1) * CHUNK_VECS && sv_tok < slice_len &&
-                        (sv_tok % CHUNK_VECS) % NCT == tid) {  // sampled-token fix-up by the owner
-                        const int h = (sv_tok % CHUNK_VECS) / NCT;
-                        if (c * VPC + h == tail_j)
-                            reinterpret_cast<__nv_bfloat16*>(drow)[tokv] = __float2bfloat16_rn(tv);
-                        else
-                            sts16_raw(slot + (h * NCT + tid) * 16 + (tokv % EPV) * 2,
-                                      __bfloat16_as_ushort(__float2bfloat16_rn(tv)));
-                    }
-                    fence_proxy_async_smem();  // the staged bytes -> visible to the TMA store
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(sbar_full + 8 * ws);
-                }
-                if (dbg) pcc.lap(dph[4]);
-                return;
-            }
             // A rolled loop (e comes from TMEM, not from indexed registers): keeps the
             // hot code small enough for the instruction caches.
 #pragma unroll 1
