@@ -249,6 +249,11 @@ __device__ __forceinline__ uint64_t ld_relaxed_cluster_u64(uint32_t addr) {
     asm volatile("ld.relaxed.cluster.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
     return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_cluster_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.relaxed.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
 __device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
     uint32_t v;

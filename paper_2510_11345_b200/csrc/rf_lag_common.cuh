@@ -82,6 +82,11 @@ __device__ __forceinline__ double combine_factor(float m, float mx) {
 #ifndef RF_PREFENCE
 #define RF_PREFENCE 0
 #endif
+// Peer-partial poll: 1 = relaxed loads + one acquire fence after the last (an acquire
+// load invalidates L1 on every poll); 0 = ld.acquire per poll (A/B knob).
+#ifndef RF_XCHG_RELAXED_POLL
+#define RF_XCHG_RELAXED_POLL 0
+#endif
 // Write phase: straight-line stores for chunks with no padded / missing vectors.
 #ifndef RF_WRITE_FAST
 #define RF_WRITE_FAST 1  // A/B on B200: +6% (per-vector branches serialised the store math)

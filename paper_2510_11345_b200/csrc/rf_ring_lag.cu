@@ -279,8 +279,13 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                         for (uint32_t q = 0; q < csize; ++q) {  // wait for every peer's partial of this row
                             if (q == rank) continue;
                             const uint32_t a = smem_u32(&xslot[(row_iter & 3) * 8 + q].seq);
-                            while (ld_acquire_cluster_u32(a) != row_iter + 1) __nanosleep(32);
+                            if (RF_XCHG_RELAXED_POLL) {
+                                while (ld_relaxed_cluster_u32(a) != row_iter + 1) __nanosleep(32);
+                            } else {
+                                while (ld_acquire_cluster_u32(a) != row_iter + 1) __nanosleep(32);
+                            }
                         }
+                        if (RF_XCHG_RELAXED_POLL) fence_acq_rel_cluster();  // one acquire for all polls
                         if (kPhaseCounters && p.dbg) pc.lap(d_x);
                     }
                     float Mx = -CUDART_INF_F;
