@@ -21,6 +21,8 @@ ap.add_argument("--launches", type=int, default=200)
 ap.add_argument("--variant", default="decoupled_ppo")
 ap.add_argument("--chunk", type=int, default=65536)
 ap.add_argument("--pool-gb", type=float, default=8)
+ap.add_argument("--random", action="store_true", help="random token ranges (1..chunk tokens) per launch")
+ap.add_argument("--seed", type=int, default=0)
 a = ap.parse_args()
 wl = S.WORKLOADS["c2"]
 rb = S.make_rank_batch(wl, 0, 1, 42, a.prompts)
@@ -46,16 +48,36 @@ threading.Thread(target=watchdog, daemon=True).start()
 ref = None
 chunks = [(t0, min(dw.T, t0 + chunk)) for t0 in range(0, dw.T, chunk)]
 t_start = time.time()
+import random  # noqa: E402
+
+rng = random.Random(a.seed)
+probe = (0, min(dw.T, 4096))  # re-run periodically: outputs must be bit-identical (race check)
+probe_sig = None
 for i in range(a.launches):
-    t0, t1 = chunks[i % len(chunks)]
+    if a.random:
+        n = rng.randint(1, chunk)
+        t0 = rng.randint(0, dw.T - n)
+        t0, t1 = t0, t0 + n
+    else:
+        t0, t1 = chunks[i % len(chunks)]
+    if i % 25 == 0:
+        t0, t1 = probe
     op.zero()
     op.run(pb, t0, t1)
     torch.cuda.synchronize()
     last[0] = time.time()
     last[1] = i
-    if i < len(chunks):
-        pass
-    if (i + 1) % 20 == 0:
-        print(f"launch {i + 1} ok ({time.time() - t_start:.1f} s), status {int(op.status.item())}", flush=True)
+    if (t0, t1) == probe:
+        sig = (op.scalars.clone().cpu(), op.dlogits[: t1 - t0].float().sum(dim=1).cpu())
+        if probe_sig is None:
+            probe_sig = sig
+        elif not (torch.equal(sig[0], probe_sig[0]) and torch.equal(sig[1], probe_sig[1])):
+            print(f"MISMATCH at launch {i}: probe outputs differ from the first run", flush=True)
+            sys.exit(2)
+    if int(op.status.item()) != 0:
+        print(f"device status {int(op.status.item())} at launch {i} ({t0}, {t1})", flush=True)
+        sys.exit(3)
+    if (i + 1) % 100 == 0:
+        print(f"launch {i + 1} ok ({time.time() - t_start:.1f} s)", flush=True)
 done[0] = True
 print("stress done", flush=True)
