@@ -95,9 +95,12 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
             const bool bf = b->logits_dtype == RF_DTYPE_BF16 && o->dlogits_dtype == RF_DTYPE_BF16;
             nvt = (bf && static_cast<int64_t>(q) * nct >= slice) ? q : 0;
         } else {
-            for (int q : (g.kind == 2 ? rf::kRingNvtLag : rf::kRingNvtSmall)) {
-                if (static_cast<int64_t>(q) * nct >= slice) {
-                    nvt = q;
+            const int* qs = g.kind == 2 ? rf::kRingNvtLag : rf::kRingNvtSmall;
+            const int nq = g.kind == 2 ? static_cast<int>(sizeof(rf::kRingNvtLag) / sizeof(int))
+                                       : static_cast<int>(sizeof(rf::kRingNvtSmall) / sizeof(int));
+            for (int i = 0; i < nq; ++i) {
+                if (static_cast<int64_t>(qs[i]) * nct >= slice) {
+                    nvt = qs[i];
                     break;
                 }
             }

@@ -23,7 +23,7 @@ constexpr size_t kRingTailBytes = 512;  // exchange / reduce / broadcast words
 // the consumers via setmaxnreg; one CTA per SM; the previous row's e parked in
 // TMEM.  Default NCW = 12 (3 consumer warps per SMSP, 152 registers each).
 constexpr int kRingWarpsLag = 12;
-constexpr int kRingNvtLag[3] = {4, 12, 25};  // instances for NCW = 12
+constexpr int kRingNvtLag[4] = {4, 11, 12, 25};  // instances for NCW = 12 (11: V = 32,000 bf16, one CTA per row)
 constexpr int kRingNvtLag8 = 38;              // NCW = 8 (experiments, bf16 only)
 constexpr int kRingNvtLag16 = 19;             // NCW = 16 (experiments, bf16 only)
 #ifndef RF_LAG_REGS_SUPPORT

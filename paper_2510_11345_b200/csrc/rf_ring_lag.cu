@@ -610,6 +610,7 @@ cudaError_t lag_cfg(const KParams& p, int ncw, int nvt, int cs, int ncl, size_t 
             case kRingNvtLag[0]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[0]>(p, cs, ncl, smem, st, maxc);
             case kRingNvtLag[1]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[1]>(p, cs, ncl, smem, st, maxc);
             case kRingNvtLag[2]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[2]>(p, cs, ncl, smem, st, maxc);
+            case kRingNvtLag[3]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[3]>(p, cs, ncl, smem, st, maxc);
         }
     }
     if (IB && OB && ncw == 8 && nvt == kRingNvtLag8) return launch_lag_t<IB, OB, 8, kRingNvtLag8>(p, cs, ncl, smem, st, maxc);
