@@ -223,6 +223,17 @@ int32_t rf_last_launch_count(void);
  * device; copies up to n counters into out and optionally resets them. */
 int32_t rf_debug_counters(uint64_t* out, int32_t n, int32_t reset);
 
+/* ---- experimental: the step before ----
+ * LM-head GEMM on the tensor cores (tcgen05) with the softmax statistics fused into
+ * its epilogue: for hidden states H [T, K] and the vocab projection W [V, K] (both
+ * bf16, row-major, K a multiple of 64, rows 16-byte aligned), writes
+ * lse[t] = log Σ_v exp((H Wᵀ)[t, v]) and x_tok[t] = (H Wᵀ)[t, token_ids[t]] (fp32)
+ * without materialising the [T, V] logits.  Device pointers, stream-ordered.
+ * No reference counterpart: the reference's policy is a logits table
+ * (policy.hpp ToyPolicy::logits); this is the fusion §8(f) names next. */
+rf_status rf_lmhead_lse(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
+                        int32_t vocab, int32_t hidden_dim, float* lse, float* x_tok, void* stream);
+
 /* ---- host API: the reference-facing call with HOST buffers ----
  * Same semantics as rf_loss_and_grad but every pointer in batch/outputs is a
  * host pointer (pinned memory recommended).  Streams the batch through the GPU

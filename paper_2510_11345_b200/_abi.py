@@ -141,6 +141,7 @@ EXPORTED_SYMBOLS = (
     "rf_last_launch_count",
     "rf_loss_and_grad_host",
     "rf_debug_counters",
+    "rf_lmhead_lse",
 )
 
 _lib = None
@@ -182,6 +183,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rf_last_launch_count.restype = _i32
     lib.rf_loss_and_grad_host.argtypes = [P(rf_loss_config), P(rf_batch), P(rf_outputs), _i32, _i64]
     lib.rf_loss_and_grad_host.restype = _i32
+    lib.rf_lmhead_lse.argtypes = [_p, _p, _p, _i64, _i32, _i32, _p, _p, _p]
+    lib.rf_lmhead_lse.restype = _i32
     lib.rf_debug_counters.argtypes = [_p, _i32, _i32]
     lib.rf_debug_counters.restype = _i32
     _lib = lib

@@ -54,6 +54,9 @@ constexpr size_t kRingKLTailBytes = 2176;  // [4][8] 40-byte exchange slots + 5 
 cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int nclusters, size_t smem,
                            cudaStream_t st);
 cudaError_t ring_kl_max_clusters(bool out_bf16, int nvt, int cs, size_t smem, int* out);
+// Experimental LM-head GEMM + fused softmax statistics (rf_lmhead.cu)
+cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
+                              float* lse, float* xtok, cudaStream_t st);
 cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
                             size_t smem, cudaStream_t st);
 cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);

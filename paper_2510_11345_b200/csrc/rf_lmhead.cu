@@ -1,0 +1,260 @@
+// rf_lmhead.cu — K0 (experimental): the LM-head GEMM on the
+// 5th-generation tensor cores with the softmax statistics fused into its epilogue,
+// so the [T, V] logits of the stats pass never reach HBM.
+//
+//   logits = H · Wᵀ      H [T, K] bf16 (hidden states), W [V, K] bf16 (vocab projection)
+//   out:   lse[t] = log Σ_v exp(logits[t, v]),  x_tok[t] = logits[t, tok_t]
+//
+// One CTA owns 128 token rows (UMMA M = 128) and sweeps the whole vocabulary in
+// 256-column tiles (UMMA N = 256), K in 64-element (128-byte, SWIZZLE_128B) chunks:
+//   warp 0      TMA producer: H and W tiles into a 4-stage shared-memory ring
+//   warp 1      one elected lane issues tcgen05.mma (kind::f16, fp32 accumulate in
+//               tensor memory), double-buffered over two 256-column TMEM accumulators
+//   warps 2-5   epilogue: tcgen05.ld of a finished tile (thread = token row), online
+//               max / Σexp in fp32 and the sampled token's logit, then release the buffer
+// The dlogits pass (a second GEMM sweep producing k·(onehot − p) tiles fed to the
+// backward GEMMs) is the next step; this kernel is the stats half, measured in TFLOP/s.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <math_constants.h>
+
+#include "rf_device.cuh"
+#include "rf_kernels.h"
+
+namespace rf {
+
+namespace {
+
+constexpr int kLmM = 128, kLmN = 256, kLmK = 64, kLmStages = 4;
+constexpr uint32_t kLmAStage = kLmM * kLmK * 2;  // 16 KB
+constexpr uint32_t kLmBStage = kLmN * kLmK * 2;  // 32 KB
+constexpr uint32_t kLmStageBytes = kLmAStage + kLmBStage;
+constexpr size_t kLmSmem = static_cast<size_t>(kLmStages) * kLmStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
+// K-major operand tile in SWIZZLE_128B layout: rows of 128 bytes, 8-row (1024 B) groups.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr & 0x3FFFFu) >> 4);  // start address
+    d |= static_cast<uint64_t>(1) << 16;                  // leading byte offset (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;          // stride byte offset: 8 rows x 128 B
+    d |= static_cast<uint64_t>(1) << 46;                  // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2) << 61;                  // layout: SWIZZLE_128B
+    return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, both K-major, M = 128, N = 256
+constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kLmN >> 3) << 17) |
+                              (static_cast<uint32_t>(kLmM >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(192, 1)
+    lmhead_lse_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
+                      const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, float* __restrict__ lse,
+                      float* __restrict__ xtok) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B tiles need 1024-byte alignment
+    const uint32_t bars = sbase + kLmStages * kLmStageBytes;
+    const uint32_t full = bars, empty = bars + 8 * kLmStages;
+    const uint32_t acc_full = bars + 16 * kLmStages, acc_empty = acc_full + 16;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (acc_empty + 16 - raw));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kLmM;
+    const int ntiles = (V + kLmN - 1) / kLmN, nk = K / kLmK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kLmStages; ++s) {
+            mbar_init(full + 8 * s, 1);
+            mbar_init(empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(acc_full + 8 * b, 1);
+            mbar_init(acc_empty + 8 * b, 4);  // the four epilogue warps
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------ TMA producer ------------------------------
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int n = 0; n < ntiles; ++n) {
+                for (int kc = 0; kc < nk; ++kc, ++it) {
+                    const uint32_t s = it % kLmStages;
+                    if (it >= static_cast<uint32_t>(kLmStages)) mbar_wait(empty + 8 * s, ((it / kLmStages) - 1) & 1);
+                    const uint32_t a = sbase + s * kLmStageBytes, b = a + kLmAStage;
+                    mbar_arrive_expect_tx(full + 8 * s, kLmStageBytes);
+                    tma_load_2d(a, &tmH, kc * kLmK, static_cast<int>(row0), full + 8 * s);
+                    tma_load_2d(b, &tmW, kc * kLmK, n * kLmN, full + 8 * s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------- MMA issuer -------------------------------
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int n = 0; n < ntiles; ++n) {
+                const uint32_t buf = n & 1;
+                if (n >= 2) mbar_wait(acc_empty + 8 * buf, ((n >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + buf * kLmN;
+                for (int kc = 0; kc < nk; ++kc, ++it) {
+                    const uint32_t s = it % kLmStages;
+                    mbar_wait(full + 8 * s, (it / kLmStages) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a = sbase + s * kLmStageBytes, b = a + kLmAStage;
+#pragma unroll
+                    for (int k = 0; k < kLmK / 16; ++k)  // UMMA K = 16: +32 bytes inside the 128-byte swizzle atom
+                        umma_f16(d, smem_desc_sw128(a + 32 * k), smem_desc_sw128(b + 32 * k), kLmIdesc,
+                                 (kc > 0 || k > 0) ? 1u : 0u);
+                    umma_commit(empty + 8 * s);  // frees the stage when these MMAs have read it
+                }
+                umma_commit(acc_full + 8 * buf);  // the tile's accumulator is complete
+            }
+        }
+    } else {
+        // -------------------------------- epilogue --------------------------------
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int64_t row = row0 + 32 * q + lane;
+        const int32_t tk = row < T ? tok[row] : -1;
+        const float L = 1.4426950408889634f;
+        float m = -CUDART_INF_F, ssum = 0.0f, xt = 0.0f;
+        for (int n = 0; n < ntiles; ++n) {
+            const uint32_t buf = n & 1;
+            mbar_wait_sleep(acc_full + 8 * buf, (n >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kLmN;
+#pragma unroll 1
+            for (int c = 0; c < kLmN; c += 32) {
+                float v[32];
+                tmem_ld32(taddr + c, v);
+                const int col0 = n * kLmN + c;
+                float cm = -CUDART_INF_F;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (col0 + i < V) cm = fmaxf(cm, v[i]);
+                const float mn = fmaxf(m, cm);
+                float acc = 0.0f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (col0 + i < V) acc += ex2_approx((v[i] - mn) * L);
+                ssum = (m == -CUDART_INF_F ? 0.0f : ssum * ex2_approx((m - mn) * L)) + acc;
+                m = mn;
+                if (tk >= col0 && tk < col0 + 32) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (tk == col0 + i) xt = v[i];
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
+        }
+        if (row < T) {
+            lse[row] = m + logf(ssum);
+            xtok[row] = xt;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kLmK), box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
+                              float* lse, float* xtok, cudaStream_t st) {
+    if (K % kLmK != 0 || T <= 0 || V <= 0) return cudaErrorInvalidValue;
+    CUtensorMap mh, mw;
+    if (!make_map(&mh, H, static_cast<uint64_t>(T), static_cast<uint64_t>(K), kLmM)) return cudaErrorInvalidValue;
+    if (!make_map(&mw, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), kLmN)) return cudaErrorInvalidValue;
+    cudaError_t e =
+        cudaFuncSetAttribute(lmhead_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kLmSmem));
+    if (e != cudaSuccess) return e;
+    const unsigned grid = static_cast<unsigned>((T + kLmM - 1) / kLmM);
+    lmhead_lse_kernel<<<grid, 192, kLmSmem, st>>>(mh, mw, tok, T, V, K, lse, xtok);
+    return cudaGetLastError();
+}
+
+}  // namespace rf
