@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <math_constants.h>
 
@@ -85,10 +86,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 }  // namespace
 
+// blockIdx.x: 128-token block; blockIdx.y: vocab split (tiles [y·tps, min(ntiles, (y+1)·tps))).
+// Writes the split's partial (max, Σexp) per token into pm/ps [gridDim.y][T]; the split
+// owning the sampled token writes x_tok directly.
 __global__ void __launch_bounds__(192, 1)
     lmhead_lse_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
-                      const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, float* __restrict__ lse,
-                      float* __restrict__ xtok) {
+                      const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
+                      float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B tiles need 1024-byte alignment
@@ -99,7 +103,9 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kLmM;
-    const int ntiles = (V + kLmN - 1) / kLmN, nk = K / kLmK;
+    const int ntiles_all = (V + kLmN - 1) / kLmN, nk = K / kLmK;
+    const int nbeg = static_cast<int>(blockIdx.y) * tps;
+    const int ntiles = max(0, min(ntiles_all, nbeg + tps) - nbeg);  // tiles of this split
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kLmStages; ++s) {
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(192, 1)
                     const uint32_t a = sbase + s * kLmStageBytes, b = a + kLmAStage;
                     mbar_arrive_expect_tx(full + 8 * s, kLmStageBytes);
                     tma_load_2d(a, &tmH, kc * kLmK, static_cast<int>(row0), full + 8 * s);
-                    tma_load_2d(b, &tmW, kc * kLmK, n * kLmN, full + 8 * s);
+                    tma_load_2d(b, &tmW, kc * kLmK, (nbeg + n) * kLmN, full + 8 * s);
                 }
             }
         }
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int c = 0; c < kLmN; c += 32) {
                 float v[32];
                 tmem_ld32(taddr + c, v);
-                const int col0 = n * kLmN + c;
+                const int col0 = (nbeg + n) * kLmN + c;
                 float cm = -CUDART_INF_F;
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
@@ -200,8 +206,9 @@ __global__ void __launch_bounds__(192, 1)
             if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
         }
         if (row < T) {
-            lse[row] = m + logf(ssum);
-            xtok[row] = xt;
+            pm[static_cast<int64_t>(blockIdx.y) * T + row] = m;
+            ps[static_cast<int64_t>(blockIdx.y) * T + row] = ssum;
+            if (tk >= nbeg * kLmN && tk < (nbeg + ntiles) * kLmN) xtok[row] = xt;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -243,6 +250,21 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
 
 }  // namespace
 
+// lse[t] = M + ln Σ_s ps[s][t]·exp(pm[s][t] - M), M = max_s pm[s][t] (fixed split order)
+__global__ void lmhead_combine_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int32_t nsplit,
+                                      int64_t T, float* __restrict__ lse) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    float M = -CUDART_INF_F;
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, pm[s * T + t]);
+    double S = 0.0;
+    for (int s = 0; s < nsplit; ++s) {
+        const float m = pm[s * T + t];
+        if (m != -CUDART_INF_F) S += static_cast<double>(ps[s * T + t]) * exp(static_cast<double>(m - M));
+    }
+    lse[t] = static_cast<float>(static_cast<double>(M) + log(S));
+}
+
 cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
                               float* lse, float* xtok, cudaStream_t st) {
     if (K % kLmK != 0 || T <= 0 || V <= 0) return cudaErrorInvalidValue;
@@ -252,9 +274,25 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
     cudaError_t e =
         cudaFuncSetAttribute(lmhead_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kLmSmem));
     if (e != cudaSuccess) return e;
-    const unsigned grid = static_cast<unsigned>((T + kLmM - 1) / kLmM);
-    lmhead_lse_kernel<<<grid, 192, kLmSmem, st>>>(mh, mw, tok, T, V, K, lse, xtok);
-    return cudaGetLastError();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // split the vocabulary so that token blocks x splits fill the SMs for ~8 waves
+    const int64_t nblk = (T + kLmM - 1) / kLmM;
+    const int ntiles = (V + kLmN - 1) / kLmN;
+    int nsplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, (8LL * sms + nblk - 1) / nblk)));
+    const int tps = (ntiles + nsplit - 1) / nsplit;
+    nsplit = (ntiles + tps - 1) / tps;
+    float* part = nullptr;
+    e = cudaMallocAsync(&part, static_cast<size_t>(2) * nsplit * T * sizeof(float), st);
+    if (e != cudaSuccess) return e;
+    lmhead_lse_kernel<<<dim3(static_cast<unsigned>(nblk), static_cast<unsigned>(nsplit)), 192, kLmSmem, st>>>(
+        mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok);
+    lmhead_combine_kernel<<<static_cast<unsigned>((T + 255) / 256), 256, 0, st>>>(
+        part, part + static_cast<size_t>(nsplit) * T, nsplit, T, lse);
+    e = cudaGetLastError();
+    cudaFreeAsync(part, st);
+    return e;
 }
 
 }  // namespace rf

@@ -1,0 +1,64 @@
+"""Throughput of the experimental LM-head GEMM + fused softmax statistics
+(rf_lmhead_lse) against cuBLAS bf16 GEMM of the same shape (logits materialised)
+followed by torch's logsumexp (run on the GPU box):
+    python tools/lmhead_bench.py [--tokens 8192] [--vocab 151936] [--hidden 4096]"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2510_11345_b200.lmhead import lmhead_lse  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--tokens", type=int, default=8192)
+ap.add_argument("--vocab", type=int, default=151936)
+ap.add_argument("--hidden", type=int, default=4096)
+ap.add_argument("--iters", type=int, default=5)
+a = ap.parse_args()
+T, V, K = a.tokens, a.vocab, a.hidden
+g = torch.Generator(device="cuda")
+g.manual_seed(0)
+H = (torch.randn(T, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+W = (torch.randn(V, K, device="cuda", generator=g) * (1.0 / K ** 0.5)).to(torch.bfloat16)
+tok = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
+flops = 2.0 * T * V * K
+
+
+def timed(fn):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / a.iters
+
+
+ms_fused = timed(lambda: lmhead_lse(H, W, tok))
+
+
+def unfused():
+    logits = H @ W.t()
+    return torch.logsumexp(logits.float(), dim=1)
+
+
+ms_gemm = timed(lambda: H @ W.t())
+ms_unfused = timed(unfused)
+peaks = {}
+try:
+    with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as f:
+        peaks = json.load(f)
+except Exception:
+    pass
+peak = float(peaks.get("bf16_tflops", peaks.get("dense_bf16_tflops", 0)) or 0)
+out = {"tokens": T, "vocab": V, "hidden": K, "fused_ms": round(ms_fused, 3),
+       "fused_tflops": round(flops / ms_fused / 1e9, 1), "cublas_gemm_ms": round(ms_gemm, 3),
+       "cublas_gemm_tflops": round(flops / ms_gemm / 1e9, 1), "cublas_gemm_plus_logsumexp_ms": round(ms_unfused, 3),
+       "logits_bytes_avoided": T * V * 2 * 2, "measured_bf16_peak_tflops": peak or None}
+print(json.dumps(out))
