@@ -234,6 +234,14 @@ int32_t rf_debug_counters(uint64_t* out, int32_t n, int32_t reset);
 rf_status rf_lmhead_lse(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
                         int32_t vocab, int32_t hidden_dim, float* lse, float* x_tok, void* stream);
 
+/* The dlogits half: recomputes the logits tiles on the tensor cores and writes
+ * dlogits[t, v] = coef[t]·(1[v = token_ids[t]] − exp((H Wᵀ)[t, v] − lse[t])) as bf16 rows
+ * of stride dlogits_row_stride (16-byte aligned rows), lse from rf_lmhead_lse and coef
+ * the per-token loss coefficient (rf_outputs.token_coef of the loss math). */
+rf_status rf_lmhead_dlogits(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
+                            int32_t vocab, int32_t hidden_dim, const float* lse, const double* coef, void* dlogits,
+                            int64_t dlogits_row_stride, void* stream);
+
 /* ---- host API: the reference-facing call with HOST buffers ----
  * Same semantics as rf_loss_and_grad but every pointer in batch/outputs is a
  * host pointer (pinned memory recommended).  Streams the batch through the GPU

@@ -142,6 +142,7 @@ EXPORTED_SYMBOLS = (
     "rf_loss_and_grad_host",
     "rf_debug_counters",
     "rf_lmhead_lse",
+    "rf_lmhead_dlogits",
 )
 
 _lib = None
@@ -185,6 +186,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rf_loss_and_grad_host.restype = _i32
     lib.rf_lmhead_lse.argtypes = [_p, _p, _p, _i64, _i32, _i32, _p, _p, _p]
     lib.rf_lmhead_lse.restype = _i32
+    lib.rf_lmhead_dlogits.argtypes = [_p, _p, _p, _i64, _i32, _i32, _p, _p, _p, _i64, _p]
+    lib.rf_lmhead_dlogits.restype = _i32
     lib.rf_debug_counters.argtypes = [_p, _i32, _i32]
     lib.rf_debug_counters.restype = _i32
     _lib = lib

@@ -525,6 +525,23 @@ rf_status rf_lmhead_lse(const void* hidden, const void* w_vocab, const int32_t* 
     return RF_OK;
 }
 
+rf_status rf_lmhead_dlogits(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
+                            int32_t vocab, int32_t hidden_dim, const float* lse, const double* coef, void* dlogits,
+                            int64_t dlogits_row_stride, void* stream) {
+    if (!hidden || !w_vocab || !token_ids || !lse || !coef || !dlogits) return RF_ERR_INVALID_ARGUMENT;
+    if (num_tokens <= 0) return RF_ERR_EMPTY_BATCH;
+    if (vocab < 2 || hidden_dim <= 0 || hidden_dim % 64 != 0 || dlogits_row_stride < vocab)
+        return RF_ERR_INVALID_ARGUMENT;
+    if (!is_aligned(hidden, 16) || !is_aligned(w_vocab, 16) || !is_aligned(dlogits, 16) ||
+        (dlogits_row_stride * 2) % 16 != 0)
+        return RF_ERR_UNSUPPORTED_LAYOUT;
+    const cudaError_t e = rf::launch_lmhead_dlogits(hidden, w_vocab, token_ids, num_tokens, vocab, hidden_dim, lse, coef,
+                                                    dlogits, dlogits_row_stride, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return RF_ERR_CUDA;
+    g_last_launches = 1;
+    return RF_OK;
+}
+
 rf_status rf_loss_and_grad(const rf_loss_config* c, const rf_batch* b, rf_outputs* o, void* stream) {
     return rf_loss_and_grad_ex(c, b, o, stream, RF_KERNEL_AUTO);
 }

@@ -57,6 +57,9 @@ cudaError_t ring_kl_max_clusters(bool out_bf16, int nvt, int cs, size_t smem, in
 // Experimental LM-head GEMM + fused softmax statistics (rf_lmhead.cu)
 cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
                               float* lse, float* xtok, cudaStream_t st);
+cudaError_t launch_lmhead_dlogits(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
+                                  const float* lse, const double* coef, void* dlogits, int64_t dl_stride,
+                                  cudaStream_t st);
 cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
                             size_t smem, cudaStream_t st);
 cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);

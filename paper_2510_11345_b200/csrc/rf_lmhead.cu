@@ -89,10 +89,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 // blockIdx.x: 128-token block; blockIdx.y: vocab split (tiles [y·tps, min(ntiles, (y+1)·tps))).
 // Writes the split's partial (max, Σexp) per token into pm/ps [gridDim.y][T]; the split
 // owning the sampled token writes x_tok directly.
+// MODE 0 (stats): partial (max, Σexp) per split + the sampled logit.
+// MODE 1 (dlogits): recompute the logits tile and write dlogit = k·(1[v = tok] − exp(x − lse))
+//         as bf16 rows of stride dl_stride (the input of the backward GEMMs); lse/coef per token.
+template <int MODE>
 __global__ void __launch_bounds__(192, 1)
-    lmhead_lse_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
-                      const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
-                      float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok) {
+    lmhead_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
+                  const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
+                  float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok,
+                  const float* __restrict__ lse_in, const double* __restrict__ coef, __nv_bfloat16* __restrict__ dl,
+                  int64_t dl_stride) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B tiles need 1024-byte alignment
@@ -174,6 +180,11 @@ __global__ void __launch_bounds__(192, 1)
         const int32_t tk = row < T ? tok[row] : -1;
         const float L = 1.4426950408889634f;
         float m = -CUDART_INF_F, ssum = 0.0f, xt = 0.0f;
+        // MODE 1: per-row constants
+        const float lseL = (MODE == 1 && row < T) ? lse_in[row] * L : 0.0f;
+        const double kd = (MODE == 1 && row < T) ? coef[row] : 0.0;
+        const float negk = static_cast<float>(-kd);
+        __nv_bfloat16* drow = (MODE == 1 && row < T) ? dl + row * dl_stride : nullptr;
         for (int n = 0; n < ntiles; ++n) {
             const uint32_t buf = n & 1;
             mbar_wait_sleep(acc_full + 8 * buf, (n >> 1) & 1);
@@ -184,6 +195,29 @@ __global__ void __launch_bounds__(192, 1)
                 float v[32];
                 tmem_ld32(taddr + c, v);
                 const int col0 = (nbeg + n) * kLmN + c;
+                if constexpr (MODE == 1) {
+                    if (drow == nullptr) continue;
+                    uint32_t w[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float o0 = negk * ex2_approx(fmaf(v[2 * i], L, -lseL));
+                        float o1 = negk * ex2_approx(fmaf(v[2 * i + 1], L, -lseL));
+                        if (kd == 0.0) o0 = o1 = 0.0f;
+                        if (tk == col0 + 2 * i) o0 = static_cast<float>(kd - kd * exp(static_cast<double>(v[2 * i]) - lse_in[row]));
+                        if (tk == col0 + 2 * i + 1)
+                            o1 = static_cast<float>(kd - kd * exp(static_cast<double>(v[2 * i + 1]) - lse_in[row]));
+                        w[i] = pack_bf16x2(o0, o1);
+                    }
+                    if (col0 + 32 <= V) {
+                        uint4* d4 = reinterpret_cast<uint4*>(drow + col0);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) d4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+                    } else {
+                        for (int i = 0; i < 32 && col0 + i < V; ++i)
+                            drow[col0 + i] = __ushort_as_bfloat16(static_cast<uint16_t>((i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xffffu)));
+                    }
+                    continue;
+                }
                 float cm = -CUDART_INF_F;
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
@@ -205,7 +239,7 @@ __global__ void __launch_bounds__(192, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
         }
-        if (row < T) {
+        if (MODE == 0 && row < T) {
             pm[static_cast<int64_t>(blockIdx.y) * T + row] = m;
             ps[static_cast<int64_t>(blockIdx.y) * T + row] = ssum;
             if (tk >= nbeg * kLmN && tk < (nbeg + ntiles) * kLmN) xtok[row] = xt;
@@ -272,7 +306,7 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
     if (!make_map(&mh, H, static_cast<uint64_t>(T), static_cast<uint64_t>(K), kLmM)) return cudaErrorInvalidValue;
     if (!make_map(&mw, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), kLmN)) return cudaErrorInvalidValue;
     cudaError_t e =
-        cudaFuncSetAttribute(lmhead_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kLmSmem));
+        cudaFuncSetAttribute(lmhead_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kLmSmem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -286,13 +320,37 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
     float* part = nullptr;
     e = cudaMallocAsync(&part, static_cast<size_t>(2) * nsplit * T * sizeof(float), st);
     if (e != cudaSuccess) return e;
-    lmhead_lse_kernel<<<dim3(static_cast<unsigned>(nblk), static_cast<unsigned>(nsplit)), 192, kLmSmem, st>>>(
-        mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok);
+    lmhead_kernel<0><<<dim3(static_cast<unsigned>(nblk), static_cast<unsigned>(nsplit)), 192, kLmSmem, st>>>(
+        mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok, nullptr, nullptr, nullptr, 0);
     lmhead_combine_kernel<<<static_cast<unsigned>((T + 255) / 256), 256, 0, st>>>(
         part, part + static_cast<size_t>(nsplit) * T, nsplit, T, lse);
     e = cudaGetLastError();
     cudaFreeAsync(part, st);
     return e;
+}
+
+cudaError_t launch_lmhead_dlogits(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
+                                  const float* lse, const double* coef, void* dlogits, int64_t dl_stride,
+                                  cudaStream_t st) {
+    if (K % kLmK != 0 || T <= 0 || V <= 0 || (dl_stride * 2) % 16 != 0) return cudaErrorInvalidValue;
+    CUtensorMap mh, mw;
+    if (!make_map(&mh, H, static_cast<uint64_t>(T), static_cast<uint64_t>(K), kLmM)) return cudaErrorInvalidValue;
+    if (!make_map(&mw, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), kLmN)) return cudaErrorInvalidValue;
+    cudaError_t e =
+        cudaFuncSetAttribute(lmhead_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kLmSmem));
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nblk = (T + kLmM - 1) / kLmM;
+    const int ntiles = (V + kLmN - 1) / kLmN;
+    int nsplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, (8LL * sms + nblk - 1) / nblk)));
+    const int tps = (ntiles + nsplit - 1) / nsplit;
+    nsplit = (ntiles + tps - 1) / tps;
+    lmhead_kernel<1><<<dim3(static_cast<unsigned>(nblk), static_cast<unsigned>(nsplit)), 192, kLmSmem, st>>>(
+        mh, mw, tok, T, V, K, tps, nullptr, nullptr, nullptr, lse, coef, static_cast<__nv_bfloat16*>(dlogits),
+        dl_stride);
+    return cudaGetLastError();
 }
 
 }  // namespace rf

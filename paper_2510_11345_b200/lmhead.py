@@ -35,3 +35,26 @@ def lmhead_lse(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch.Ten
 
         raise RuntimeError(f"rf_lmhead_lse: {status_string(st)}")
     return lse, xt
+
+
+def lmhead_dlogits(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch.Tensor, lse: torch.Tensor,
+                   coef: torch.Tensor, stream=None) -> torch.Tensor:
+    """dlogits[t, v] = coef[t]·(1[v = tok_t] − exp((H Wᵀ)[t, v] − lse[t])), bf16, from a second
+    tensor-core sweep (the logits are recomputed, never stored)."""
+    T, K = hidden.shape
+    V = w_vocab.shape[0]
+    padV = (V + 7) // 8 * 8
+    out = torch.empty(T, padV, dtype=torch.bfloat16, device=hidden.device)
+    tok = token_ids.to(device=hidden.device, dtype=torch.int32).contiguous()
+    lse32 = lse.to(torch.float32).contiguous()
+    c64 = coef.to(torch.float64).contiguous()
+    lib = _abi.load_library()
+    s = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    st = lib.rf_lmhead_dlogits(hidden.data_ptr(), w_vocab.data_ptr(), tok.data_ptr(), T, V, K, lse32.data_ptr(),
+                               c64.data_ptr(), out.data_ptr(), padV, s)
+    if st != 0:
+        from .losses import status_string
+
+        raise RuntimeError(f"rf_lmhead_dlogits: {status_string(st)}")
+    return out[:, :V]

@@ -5,7 +5,7 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-from paper_2510_11345_b200.lmhead import lmhead_lse  # noqa: E402
+from paper_2510_11345_b200.lmhead import lmhead_dlogits, lmhead_lse  # noqa: E402
 
 
 def _ref(H, W, tok):
@@ -26,3 +26,26 @@ def test_lmhead_lse_matches_torch(T, V, K):
     # fp32 accumulation in a different order + ex2.approx: absolute tolerance in log space
     assert torch.allclose(xt.double(), rx, atol=2e-3, rtol=1e-4), (xt - rx).abs().max()
     assert torch.allclose(lse.double(), rl, atol=2e-3, rtol=1e-5), (lse.double() - rl).abs().max()
+
+
+@pytest.mark.parametrize("T,V,K", [(128, 256, 64), (300, 1003, 256), (256, 151936, 4096)])
+def test_lmhead_dlogits_matches_torch(T, V, K):
+    """The dlogits sweep: coef·(onehot − softmax) from recomputed logits, using the stats
+    kernel's lse; against the fp32 torch reference, at the north-star dlogit tolerance."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(T + 3 * V + K)
+    H = (torch.randn(T, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(V, K, device="cuda", generator=g) * (1.0 / K ** 0.5)).to(torch.bfloat16)
+    tok = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
+    coef = torch.randn(T, device="cuda", generator=g, dtype=torch.float64) * 1e-3
+    coef[::7] = 0.0
+    lse, _ = lmhead_lse(H, W, tok)
+    dl = lmhead_dlogits(H, W, tok, lse, coef)
+    torch.cuda.synchronize()
+    logits = (H.float() @ W.float().t()).double()
+    p = torch.softmax(logits, dim=1)
+    ref = -coef[:, None] * p
+    ref[torch.arange(T, device="cuda"), tok.long()] += coef
+    err = (dl.double() - ref).abs()
+    bound = 2e-3 * coef.abs()[:, None] + 2.0 ** -8 * ref.abs() + 1e-30
+    assert bool((err <= bound).all()), float((err / bound).max())
