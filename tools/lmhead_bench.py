@@ -10,7 +10,7 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2510_11345_b200.lmhead import lmhead_lse  # noqa: E402
+from paper_2510_11345_b200.lmhead import lmhead_dlogits, lmhead_lse  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--tokens", type=int, default=8192)
@@ -48,7 +48,21 @@ def unfused():
     return torch.logsumexp(logits.float(), dim=1)
 
 
+lse0, _ = lmhead_lse(H, W, tok)
+coef = torch.full((T,), 1e-4, dtype=torch.float64, device="cuda")
+ms_dl = timed(lambda: lmhead_dlogits(H, W, tok, lse0, coef))
+
+
+def unfused_dl():
+    logits = H @ W.t()
+    p = torch.softmax(logits.float(), dim=1)
+    d = (-coef[:, None].float() * p)
+    d[torch.arange(T, device="cuda"), tok.long()] += coef.float()
+    return d.to(torch.bfloat16)
+
+
 ms_gemm = timed(lambda: H @ W.t())
+ms_unfused_dl = timed(unfused_dl) if T * V <= 8192 * 151936 else None
 ms_unfused = timed(unfused)
 peaks = {}
 try:
@@ -60,5 +74,8 @@ peak = float(peaks.get("bf16_tflops", peaks.get("dense_bf16_tflops", 0)) or 0)
 out = {"tokens": T, "vocab": V, "hidden": K, "fused_ms": round(ms_fused, 3),
        "fused_tflops": round(flops / ms_fused / 1e9, 1), "cublas_gemm_ms": round(ms_gemm, 3),
        "cublas_gemm_tflops": round(flops / ms_gemm / 1e9, 1), "cublas_gemm_plus_logsumexp_ms": round(ms_unfused, 3),
-       "logits_bytes_avoided": T * V * 2 * 2, "measured_bf16_peak_tflops": peak or None}
+       "logits_bytes_avoided": T * V * 2 * 2, "measured_bf16_peak_tflops": peak or None,
+       "fused_dlogits_ms": round(ms_dl, 3), "fused_dlogits_tflops": round(flops / ms_dl / 1e9, 1),
+       "fused_stats_plus_dlogits_ms": round(ms_fused + ms_dl, 3),
+       "cublas_gemm_plus_torch_softmax_dlogits_ms": None if ms_unfused_dl is None else round(ms_unfused_dl, 3)}
 print(json.dumps(out))
