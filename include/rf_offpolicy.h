@@ -242,6 +242,13 @@ rf_status rf_lmhead_dlogits(const void* hidden, const void* w_vocab, const int32
                             int32_t vocab, int32_t hidden_dim, const float* lse, const double* coef, void* dlogits,
                             int64_t dlogits_row_stride, void* stream);
 
+/* The per-token loss math between the two LM-head sweeps: lp = x_tok − lse, then the
+ * surrogate, coefficient, clip flags and scalars of rf_loss_and_grad (token_mean
+ * aggregation, no exact KL; batch->logits is not read).  outputs->token_coef feeds
+ * rf_lmhead_dlogits; outputs->scalars accumulates like rf_loss_and_grad. */
+rf_status rf_token_loss_from_stats(const rf_loss_config* cfg, const rf_batch* batch, const float* lse,
+                                   const float* x_tok, rf_outputs* outputs, void* stream);
+
 /* ---- host API: the reference-facing call with HOST buffers ----
  * Same semantics as rf_loss_and_grad but every pointer in batch/outputs is a
  * host pointer (pinned memory recommended).  Streams the batch through the GPU

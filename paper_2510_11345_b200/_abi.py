@@ -143,6 +143,7 @@ EXPORTED_SYMBOLS = (
     "rf_debug_counters",
     "rf_lmhead_lse",
     "rf_lmhead_dlogits",
+    "rf_token_loss_from_stats",
 )
 
 _lib = None
@@ -188,6 +189,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rf_lmhead_lse.restype = _i32
     lib.rf_lmhead_dlogits.argtypes = [_p, _p, _p, _i64, _i32, _i32, _p, _p, _p, _i64, _p]
     lib.rf_lmhead_dlogits.restype = _i32
+    lib.rf_token_loss_from_stats.argtypes = [P(rf_loss_config), P(rf_batch), _p, _p, P(rf_outputs), _p]
+    lib.rf_token_loss_from_stats.restype = _i32
     lib.rf_debug_counters.argtypes = [_p, _i32, _i32]
     lib.rf_debug_counters.restype = _i32
     _lib = lib

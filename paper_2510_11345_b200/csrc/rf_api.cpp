@@ -198,7 +198,9 @@ int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t s
 
 int generic_grid(int64_t T) { return static_cast<int>(std::min<int64_t>(T, rf::kGenericMaxGrid)); }
 
-int64_t partial_rows(const rf_batch* b) { return std::max<int64_t>(rf::kGenericMaxGrid, b->num_seqs); }
+int64_t partial_rows(const rf_batch* b) {
+    return std::max<int64_t>(std::max<int64_t>(rf::kGenericMaxGrid, b->num_seqs), (b->num_tokens + 255) / 256);
+}
 
 struct WsLayout {
     double* partials = nullptr;
@@ -539,6 +541,65 @@ rf_status rf_lmhead_dlogits(const void* hidden, const void* w_vocab, const int32
                                                     dlogits, dlogits_row_stride, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return RF_ERR_CUDA;
     g_last_launches = 1;
+    return RF_OK;
+}
+
+rf_status rf_token_loss_from_stats(const rf_loss_config* c, const rf_batch* b, const float* lse, const float* x_tok,
+                                   rf_outputs* o, void* stream) {
+    g_last_launches = 0;
+    if (!c || !b || !o || !lse || !x_tok) return RF_ERR_INVALID_ARGUMENT;
+    rf_status st = rf_loss_config_validate(c);
+    if (st != RF_OK) return st;
+    if (b->num_tokens <= 0 || b->num_seqs <= 0) return RF_ERR_EMPTY_BATCH;
+    if (c->aggregation != RF_TOKEN_MEAN || (c->variant == RF_GRPO && c->kl_weight > 0.0))
+        return RF_ERR_INVALID_ARGUMENT;  // token_mean without exact KL (a per-token row sum is not available here)
+    if (c->variant == RF_DECOUPLED_PPO && !b->prox_logp) return RF_ERR_MISSING_PROX;
+    if (c->engine_mismatch_cap > 0.0 && !b->engine_logp) return RF_ERR_MISSING_ENGINE_LOGP;
+    if (!b->token_ids || !b->seq_of_token || !b->seq_offsets || !b->advantages || !b->behavior_logp)
+        return RF_ERR_INVALID_ARGUMENT;
+    if (!o->scalars || !o->device_status) return RF_ERR_INVALID_ARGUMENT;
+    if (b->logp_dtype != RF_DTYPE_F32 && b->logp_dtype != RF_DTYPE_F64) return RF_ERR_INVALID_ARGUMENT;
+    if (b->normalization == RF_NORM_SEQ_THEN_BATCH && b->global_num_seqs <= 0) return RF_ERR_INVALID_ARGUMENT;
+    if (b->normalization == RF_NORM_GLOBAL_TOKEN && b->global_num_tokens <= 0) return RF_ERR_INVALID_ARGUMENT;
+    const WsLayout ws = ws_layout(c, b, o->workspace);
+    if (!o->workspace || o->workspace_bytes < ws.bytes) return RF_ERR_WORKSPACE_TOO_SMALL;
+    KParams p{};
+    p.variant = c->variant;
+    p.aggregation = c->aggregation;
+    p.clip_eps = c->clip_eps;
+    p.eps_low = c->eps_low;
+    p.eps_high = c->eps_high;
+    p.trunc_cap = c->trunc_cap;
+    p.kl_weight = c->kl_weight;
+    p.w_plus = c->w_plus;
+    p.w_minus = c->w_minus;
+    p.mismatch_cap = c->engine_mismatch_cap;
+    p.T = b->num_tokens;
+    p.V = b->vocab;
+    p.logp_f64 = b->logp_dtype == RF_DTYPE_F64 ? 1 : 0;
+    p.token_ids = b->token_ids;
+    p.seq_of_token = b->seq_of_token;
+    p.seq_offsets = b->seq_offsets;
+    p.advantages = b->advantages;
+    p.behavior_logp = b->behavior_logp;
+    p.prox_logp = b->prox_logp;
+    p.engine_logp = b->engine_logp;
+    p.normalization = b->normalization;
+    p.inv_n = b->global_num_seqs > 0 ? 1.0 / static_cast<double>(b->global_num_seqs) : 0.0;
+    p.inv_t = b->global_num_tokens > 0 ? 1.0 / static_cast<double>(b->global_num_tokens) : 0.0;
+    p.grad_sign = b->grad_sign;
+    p.token_logp = o->token_logp;
+    p.token_ratio = o->token_ratio;
+    p.token_coef = o->token_coef;
+    p.token_loss = o->token_loss;
+    p.token_flags = o->token_flags;
+    p.status = o->device_status;
+    p.partials = ws.partials;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (rf::launch_token_loss(p, lse, x_tok, s) != cudaSuccess) return RF_ERR_CUDA;
+    if (rf::launch_finalize(ws.partials, (b->num_tokens + 255) / 256, o->scalars, s) != cudaSuccess)
+        return RF_ERR_CUDA;
+    g_last_launches = 2;
     return RF_OK;
 }
 

@@ -349,6 +349,58 @@ __global__ void seq_kernel(const __grid_constant__ KParams p, int64_t seq_begin,
 }
 
 // ===========================================================================
+// K2t: per-token loss math from log-probs given as lse and the sampled logit
+// (the LM-head path: lp = x_tok − lse, no logits row).  One thread per token,
+// reference semantics (token_math, losses.cpp:262-320); per-block partial rows
+// in a fixed tree order.
+// ===========================================================================
+__global__ void __launch_bounds__(256) token_loss_kernel(const __grid_constant__ KParams p,
+                                                         const float* __restrict__ lse,
+                                                         const float* __restrict__ xtok) {
+    __shared__ double sh[RF_NUM_SCALARS][256];
+    Partials part;
+    part.zero();
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+    if (t < p.T) {
+        const int32_t tok = p.token_ids[t];
+        TokenResult tr;
+        double lp = CUDART_NAN;
+        if (tok < 0 || tok >= p.V) {
+            atomicOr(p.status, RF_DEVSTAT_TOKEN_OUT_OF_RANGE);
+            tr.ratio = CUDART_NAN;
+            tr.k = 0.0;
+            tr.loss = 0.0;
+            tr.flags = RF_FLAG_NONFINITE | RF_FLAG_ZERO_COEF;
+        } else {
+            lp = static_cast<double>(xtok[t]) - static_cast<double>(lse[t]);
+            tr = token_math(p, t, lp, p.seq_of_token[t]);
+            if (tr.flags & RF_FLAG_NONFINITE) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
+        }
+        if (p.token_logp) p.token_logp[t] = lp;
+        if (p.token_ratio) p.token_ratio[t] = tr.ratio;
+        if (p.token_coef) p.token_coef[t] = tr.k;
+        if (p.token_loss) p.token_loss[t] = tr.loss;
+        if (p.token_flags) p.token_flags[t] = static_cast<uint8_t>(tr.flags);
+        part.add_token(tr, 0.0);
+    }
+    for (int j = 0; j < RF_NUM_SCALARS; ++j) sh[j][threadIdx.x] = part.v[j];
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int j = 0; j < RF_NUM_SCALARS; ++j) sh[j][threadIdx.x] += sh[j][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int j = 0; j < RF_NUM_SCALARS; ++j) p.partials[static_cast<size_t>(blockIdx.x) * RF_NUM_SCALARS + j] = sh[j][0];
+}
+
+cudaError_t launch_token_loss(const KParams& p, const float* lse, const float* xtok, cudaStream_t st) {
+    const int grid = static_cast<int>((p.T + 255) / 256);
+    token_loss_kernel<<<grid, 256, 0, st>>>(p, lse, xtok);
+    return cudaGetLastError();
+}
+
+// ===========================================================================
 // K3: scalars[j] += sum_i partials[i][j] in a fixed order (deterministic).
 // ===========================================================================
 __global__ void finalize_kernel(const double* __restrict__ partials, int64_t n, double* __restrict__ scalars) {

@@ -73,6 +73,7 @@ cudaError_t launch_generic(const KParams& p, bool in_bf16, bool out_bf16, int gr
 // K2w (rf_stream.cu): dlogits from per-token coef + lse (needs p.row_vecs, ring-compatible layout)
 cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st);
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st);
+cudaError_t launch_token_loss(const KParams& p, const float* lse, const float* xtok, cudaStream_t st);
 cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, cudaStream_t st);
 cudaError_t launch_grpo(const double* rewards, const int64_t* group_offsets, int64_t num_groups, double* adv,
                         uint8_t* degenerate, int32_t* status, cudaStream_t st);

@@ -58,3 +58,49 @@ def lmhead_dlogits(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch
 
         raise RuntimeError(f"rf_lmhead_dlogits: {status_string(st)}")
     return out[:, :V]
+
+
+def lmhead_loss_and_grad(config, hidden: torch.Tensor, w_vocab: torch.Tensor, batch, stream=None):
+    """The off-policy loss and dlogits from hidden states, logits never materialised:
+    tensor-core stats sweep (lse, sampled logit) -> per-token loss math
+    (``rf_token_loss_from_stats``, reference semantics) -> tensor-core dlogits sweep.
+
+    ``batch`` is a ``losses.PackedBatch`` whose ``logits`` is only a placeholder
+    (``vocab`` must be set); token_mean aggregation, no exact KL.  Returns a
+    ``losses.LossResult`` (dlogits bf16 [T, V])."""
+    import ctypes
+
+    from . import losses as L
+
+    config.validate()
+    dev = hidden.device
+    T = batch.num_tokens
+    lse, xt = lmhead_lse(hidden, w_vocab, batch.token_ids, stream)
+    f64 = torch.float64
+    out = {k: torch.empty(T, dtype=f64, device=dev) for k in ("lp", "ratio", "coef", "loss")}
+    flags = torch.empty(T, dtype=torch.uint8, device=dev)
+    scalars = torch.zeros(_abi.RF_NUM_SCALARS, dtype=f64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    cfg_c = config.to_c()
+    b = batch.to_c(0, T)
+    lib = _abi.load_library()
+    wsb = lib.rf_workspace_bytes(ctypes.byref(cfg_c), ctypes.byref(b))
+    ws = torch.empty(max(int(wsb), 256), dtype=torch.uint8, device=dev)
+    o = _abi.rf_outputs()
+    o.token_logp, o.token_ratio = out["lp"].data_ptr(), out["ratio"].data_ptr()
+    o.token_coef, o.token_loss, o.token_flags = out["coef"].data_ptr(), out["loss"].data_ptr(), flags.data_ptr()
+    o.scalars, o.device_status = scalars.data_ptr(), status.data_ptr()
+    o.workspace, o.workspace_bytes = ws.data_ptr(), ws.numel()
+    s = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    st = lib.rf_token_loss_from_stats(ctypes.byref(cfg_c), ctypes.byref(b), lse.data_ptr(), xt.data_ptr(),
+                                      ctypes.byref(o), s)
+    if st != 0:
+        raise L.InvalidArgument(L.status_string(st))
+    dl = lmhead_dlogits(hidden, w_vocab, batch.token_ids, lse, out["coef"], stream)
+    torch.cuda.synchronize(dev)
+    dst = int(status.item())
+    if dst & _abi.RF_DEVSTAT_NONFINITE_RATIO:
+        raise L.InvalidArgument(L.status_string(_abi.RF_ERR_NONFINITE_RATIO))
+    return L.LossResult(scalars=scalars, dlogits=dl, token_logp=out["lp"], token_ratio=out["ratio"],
+                        token_coef=out["coef"], token_loss=out["loss"], token_flags=flags)
