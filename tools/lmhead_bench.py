@@ -64,6 +64,34 @@ def unfused_dl():
 ms_gemm = timed(lambda: H @ W.t())
 ms_unfused_dl = timed(unfused_dl) if T * V <= 8192 * 151936 else None
 ms_unfused = timed(unfused)
+# End-to-end loss + dlogits from hidden states: the fused pipeline (two tensor-core sweeps,
+# no logits tensor) against cuBLAS logits (materialised, bf16) + the fused ring loss kernel.
+import paper_2510_11345_b200 as rf  # noqa: E402
+from paper_2510_11345_b200 import losses as L  # noqa: E402
+from paper_2510_11345_b200.lmhead import lmhead_loss_and_grad  # noqa: E402
+
+L_seq = 8
+nseq = T // L_seq
+seq_offsets = torch.arange(0, nseq + 1, device="cuda", dtype=torch.int64) * L_seq
+lse_r, xt_r = lmhead_lse(H, W, tok)
+lp0 = (xt_r - lse_r).double()
+behavior = (lp0 - 0.05 * torch.randn(T, device="cuda", generator=g, dtype=torch.float64)).float()
+adv = torch.randn(nseq, device="cuda", generator=g, dtype=torch.float64)
+logits_buf = torch.empty(T, (V + 7) // 8 * 8, dtype=torch.bfloat16, device="cuda")[:, :V]
+pb = L.PackedBatch(logits=logits_buf, token_ids=tok, seq_offsets=seq_offsets, advantages=adv, behavior_logp=behavior,
+                   normalization=L.Normalization.global_token)
+cfg = L.LossConfig()  # PPO-clip
+op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=T)
+
+
+def composed():
+    torch.matmul(H, W.t(), out=logits_buf)
+    op.zero()
+    op.run(pb, 0, T)
+
+
+ms_composed = timed(composed)
+ms_pipeline = timed(lambda: lmhead_loss_and_grad(cfg, H, W, pb))
 peaks = {}
 try:
     with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as f:
@@ -77,5 +105,7 @@ out = {"tokens": T, "vocab": V, "hidden": K, "fused_ms": round(ms_fused, 3),
        "logits_bytes_avoided": T * V * 2 * 2, "measured_bf16_peak_tflops": peak or None,
        "fused_dlogits_ms": round(ms_dl, 3), "fused_dlogits_tflops": round(flops / ms_dl / 1e9, 1),
        "fused_stats_plus_dlogits_ms": round(ms_fused + ms_dl, 3),
-       "cublas_gemm_plus_torch_softmax_dlogits_ms": None if ms_unfused_dl is None else round(ms_unfused_dl, 3)}
+       "cublas_gemm_plus_torch_softmax_dlogits_ms": None if ms_unfused_dl is None else round(ms_unfused_dl, 3),
+       "loss_and_dlogits_fused_pipeline_ms": round(ms_pipeline, 3),
+       "loss_and_dlogits_cublas_logits_plus_ring_kernel_ms": round(ms_composed, 3)}
 print(json.dumps(out))
