@@ -6,17 +6,19 @@
 // in the register file during the exp sweep), but the consumer warps never wait
 // for the row coefficient of the row they just reduced:
 //
-//   row i   : copy-in + max + exp sweep in registers -> partial (M,S) -> scalar warp
-//             e_i parked in TENSOR MEMORY (tcgen05.st, 120 columns per thread)
-//   row i+1 : copy-in + max + exp sweep in registers -> partial -> scalar warp
-//   row i   : wait k_i (computed by the scalar warp while row i+1 streamed in),
+//   row i   : copy-in + max + exp sweep in registers -> warp partials (M,S) -> scalar warp
+//   row i+1 : copy-in (parking e_i in TENSOR MEMORY chunk by chunk, tcgen05.st,
+//             4·NVT columns per thread) + max + exp sweep -> partials -> scalar warp
+//   row i   : wait k_i (computed by a scalar warp while row i+1 streamed in),
 //             read e_i back from TMEM (tcgen05.ld) and write its dlogits
 //
 // TMEM (256 KB per SM, unused by this non-GEMM path) is the second row buffer
-// next to the register file; the scalar warp (DSMEM cluster exchange + fp64
-// surrogate math, losses.cpp:264-320) has a whole row of streaming to finish.
-// One CTA per SM (12 warps: 10 consumers, 1 TMA producer, 1 scalar), 2-CTA
-// clusters for the Qwen3 vocabulary.
+// next to the register file; the scalar warps (DSMEM cluster exchange + fp64
+// surrogate math, losses.cpp:264-320) have a whole row of streaming to finish.
+// One CTA per SM: 12 consumer warps (152 registers via setmaxnreg) + one support
+// warpgroup (TMA producer, two scalar warps for even/odd rows, one idle warp);
+// 2-CTA clusters for the Qwen3 vocabulary.  Build-time A/B knobs and their measured
+// outcomes: rf_lag_common.cuh, profiles/r01_ab/ab_log.txt.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
