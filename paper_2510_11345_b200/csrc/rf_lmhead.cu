@@ -86,7 +86,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 }  // namespace
 
-// blockIdx.x: 128-token block; blockIdx.y: vocab split (tiles [y·tps, min(ntiles, (y+1)·tps))).
+// Grouped raster over (128-token block, vocab split): panels of `group` token blocks; inside a
+// panel the token blocks vary fastest, so the CTAs resident together share W tiles (streamed in
+// step) and the panel's H blocks (group·128·K·2 bytes) stay L2-resident.  Split x covers vocab
+// tiles [x·tps, min(ntiles, (x+1)·tps)).
 // Writes the split's partial (max, Σexp) per token into pm/ps [gridDim.y][T]; the split
 // owning the sampled token writes x_tok directly.
 // MODE 0 (stats): partial (max, Σexp) per split + the sampled logit.
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(192, 1)
                   const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
                   float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok,
                   const float* __restrict__ lse_in, const double* __restrict__ coef, __nv_bfloat16* __restrict__ dl,
-                  int64_t dl_stride) {
+                  int64_t dl_stride, int32_t nsplit, int32_t group) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B tiles need 1024-byte alignment
@@ -108,9 +111,15 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (acc_empty + 16 - raw));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kLmM;
+    const int64_t nblk = (T + kLmM - 1) / kLmM;
+    const int64_t per_panel = static_cast<int64_t>(group) * nsplit;
+    const int64_t panel = blockIdx.x / per_panel, in_panel = blockIdx.x % per_panel;
+    const int64_t g0 = panel * group, gsz = (nblk - g0 < group) ? (nblk - g0) : static_cast<int64_t>(group);
+    const int64_t blk = g0 + in_panel % gsz;
+    const int split = static_cast<int>(in_panel / gsz);
+    const int64_t row0 = blk * kLmM;
     const int ntiles_all = (V + kLmN - 1) / kLmN, nk = K / kLmK;
-    const int nbeg = static_cast<int>(blockIdx.y) * tps;
+    const int nbeg = split * tps;
     const int ntiles = max(0, min(ntiles_all, nbeg + tps) - nbeg);  // tiles of this split
 
     if (threadIdx.x == 0) {
@@ -240,8 +249,8 @@ __global__ void __launch_bounds__(192, 1)
             if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
         }
         if (MODE == 0 && row < T) {
-            pm[static_cast<int64_t>(blockIdx.y) * T + row] = m;
-            ps[static_cast<int64_t>(blockIdx.y) * T + row] = ssum;
+            pm[static_cast<int64_t>(split) * T + row] = m;
+            ps[static_cast<int64_t>(split) * T + row] = ssum;
             if (tk >= nbeg * kLmN && tk < (nbeg + ntiles) * kLmN) xtok[row] = xt;
         }
     }
@@ -268,6 +277,12 @@ EncodeFn encode_fn() {
             fn = reinterpret_cast<EncodeFn>(p);
     }
     return fn;
+}
+
+// token blocks per raster panel: their H blocks (128·K·2 bytes each) within ~64 MB of L2
+int lm_group(int64_t nblk, int32_t K) {
+    const int64_t per = static_cast<int64_t>(kLmM) * K * 2;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nblk, (64LL << 20) / per)));
 }
 
 bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
@@ -320,8 +335,10 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
     float* part = nullptr;
     e = cudaMallocAsync(&part, static_cast<size_t>(2) * nsplit * T * sizeof(float), st);
     if (e != cudaSuccess) return e;
-    lmhead_kernel<0><<<dim3(static_cast<unsigned>(nblk), static_cast<unsigned>(nsplit)), 192, kLmSmem, st>>>(
-        mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok, nullptr, nullptr, nullptr, 0);
+    const int group = lm_group(nblk, K);
+    lmhead_kernel<0><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
+        mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok, nullptr, nullptr, nullptr, 0,
+        nsplit, group);
     lmhead_combine_kernel<<<static_cast<unsigned>((T + 255) / 256), 256, 0, st>>>(
         part, part + static_cast<size_t>(nsplit) * T, nsplit, T, lse);
     e = cudaGetLastError();
@@ -347,9 +364,10 @@ cudaError_t launch_lmhead_dlogits(const void* H, const void* W, const int32_t* t
     int nsplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, (8LL * sms + nblk - 1) / nblk)));
     const int tps = (ntiles + nsplit - 1) / nsplit;
     nsplit = (ntiles + tps - 1) / tps;
-    lmhead_kernel<1><<<dim3(static_cast<unsigned>(nblk), static_cast<unsigned>(nsplit)), 192, kLmSmem, st>>>(
+    const int group = lm_group(nblk, K);
+    lmhead_kernel<1><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
         mh, mw, tok, T, V, K, tps, nullptr, nullptr, nullptr, lse, coef, static_cast<__nv_bfloat16*>(dlogits),
-        dl_stride);
+        dl_stride, nsplit, group);
     return cudaGetLastError();
 }
 
