@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(192, 1)
         const double kd = (MODE == 1 && row < T) ? coef[row] : 0.0;
         const float negk = static_cast<float>(-kd);
         __nv_bfloat16* drow = (MODE == 1 && row < T) ? dl + row * dl_stride : nullptr;
+        const bool st256 = MODE == 1 && (dl_stride * 2) % 32 == 0 && (reinterpret_cast<uintptr_t>(dl) & 31) == 0;
         for (int n = 0; n < ntiles; ++n) {
             const uint32_t buf = n & 1;
             mbar_wait_sleep(acc_full + 8 * buf, (n >> 1) & 1);
@@ -218,9 +219,20 @@ __global__ void __launch_bounds__(192, 1)
                         w[i] = pack_bf16x2(o0, o1);
                     }
                     if (col0 + 32 <= V) {
-                        uint4* d4 = reinterpret_cast<uint4*>(drow + col0);
+                        if (st256) {  // two full 32-byte sectors per thread (STG.256)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) d4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+                            for (int i = 0; i < 2; ++i)
+                                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(
+                                                 drow + col0 + 16 * i),
+                                             "r"(w[8 * i]), "r"(w[8 * i + 1]), "r"(w[8 * i + 2]), "r"(w[8 * i + 3]),
+                                             "r"(w[8 * i + 4]), "r"(w[8 * i + 5]), "r"(w[8 * i + 6]), "r"(w[8 * i + 7])
+                                             : "memory");
+                        } else {
+                            uint4* d4 = reinterpret_cast<uint4*>(drow + col0);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                d4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+                        }
                     } else {
                         for (int i = 0; i < 32 && col0 + i < V; ++i)
                             drow[col0 + i] = __ushort_as_bfloat16(static_cast<uint16_t>((i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xffffu)));
