@@ -23,15 +23,21 @@ ap.add_argument("--chunk", type=int, default=65536)
 ap.add_argument("--pool-gb", type=float, default=8)
 ap.add_argument("--random", action="store_true", help="random token ranges (1..chunk tokens) per launch")
 ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--kl", action="store_true", help="exact-KL GRPO (a reference-policy pool row per token)")
 a = ap.parse_args()
 wl = S.WORKLOADS["c2"]
 rb = S.make_rank_batch(wl, 0, 1, 42, a.prompts)
 dw = S.DeviceWorkload(rb, wl.vocab, pool_gb=a.pool_gb, device="cuda")
+ref = None
+if a.kl:
+    padV = (wl.vocab + 7) // 8 * 8
+    ref = (torch.randn(dw.pool_rows, padV, device="cuda") * 2.0).to(torch.bfloat16)[:, : wl.vocab]
 pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_offsets, advantages=dw.advantages,
                    behavior_logp=dw.behavior_logp, row_of_token=dw.row_of_token, prox_logp=dw.prox_logp,
-                   engine_logp=dw.engine_logp, normalization=L.Normalization.global_token)
+                   engine_logp=dw.engine_logp, normalization=L.Normalization.global_token, ref_logits=ref)
 chunk = min(a.chunk, dw.T)
-op = rf.OffPolicyLoss(L.LossConfig() if a.variant == "ppo" else config(a.variant), pb, chunk_tokens=chunk)
+cfg = config("grpo", kl_weight=0.1) if a.kl else (L.LossConfig() if a.variant == "ppo" else config(a.variant))
+op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=chunk)
 last = [time.time(), 0]
 done = [False]
 
