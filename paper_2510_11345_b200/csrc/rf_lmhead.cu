@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <math_constants.h>
 
@@ -273,6 +274,183 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// 2-CTA stats sweep (default; RF_LMHEAD_2CTA=0 selects lmhead_kernel<0>): a cluster pair computes a
+// 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256, N = 256); each CTA stages its
+// own 128 H rows and half (128 rows) of the W tile, so operand traffic per FLOP halves.
+// The leader (rank 0) issues the MMAs; its full barriers collect both CTAs' TMA bytes;
+// commits multicast to both CTAs; each CTA's epilogue reads its own 128 accumulator
+// rows and releases the buffer on the leader's barrier.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kL2Stages = 6;
+constexpr uint32_t kL2AStage = 128 * kLmK * 2, kL2BStage = 128 * kLmK * 2;  // 16 KB + 16 KB
+constexpr uint32_t kL2StageBytes = kL2AStage + kL2BStage;
+constexpr size_t kL2Smem = static_cast<size_t>(kL2Stages) * kL2StageBytes + 1024 + 256;
+constexpr uint32_t kL2Idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(256 >> 3) << 17) |
+                              (static_cast<uint32_t>(256 >> 4) << 24);
+
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(192, 1)
+    lmhead2_stats_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
+                         const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
+                         float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok, int32_t nsplit,
+                         int32_t group) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;
+    const uint32_t bars = sbase + kL2Stages * kL2StageBytes;
+    const uint32_t full = bars, empty = bars + 8 * kL2Stages;
+    const uint32_t acc_full = bars + 16 * kL2Stages, acc_empty = acc_full + 16;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (acc_empty + 16 - raw));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    // (256-token pair block, vocab split) of this cluster, grouped raster as in lmhead_kernel
+    const int64_t nblk = (T + 255) / 256;
+    const int64_t cidx = blockIdx.x >> 1;
+    const int64_t per_panel = static_cast<int64_t>(group) * nsplit;
+    const int64_t panel = cidx / per_panel, in_panel = cidx % per_panel;
+    const int64_t g0 = panel * group, gsz = (nblk - g0 < group) ? (nblk - g0) : static_cast<int64_t>(group);
+    const int64_t blk = g0 + in_panel % gsz;
+    const int split = static_cast<int>(in_panel / gsz);
+    const int64_t row0 = blk * 256 + 128 * rank;
+    const int ntiles_all = (V + kLmN - 1) / kLmN, nk = K / kLmK;
+    const int nbeg = split * tps;
+    const int ntiles = max(0, min(ntiles_all, nbeg + tps) - nbeg);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kL2Stages; ++s) {
+            mbar_init(full + 8 * s, 1);
+            mbar_init(empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(acc_full + 8 * b, 1);
+            mbar_init(acc_empty + 8 * b, 8);  // four epilogue warps in each CTA of the pair
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer (both CTAs): own H rows + own half of the W tile
+            uint32_t it = 0;
+            for (int n = 0; n < ntiles; ++n) {
+                for (int kc = 0; kc < nk; ++kc, ++it) {
+                    const uint32_t s = it % kL2Stages;
+                    if (it >= static_cast<uint32_t>(kL2Stages)) mbar_wait(empty + 8 * s, ((it / kL2Stages) - 1) & 1);
+                    const uint32_t a = sbase + s * kL2StageBytes, b = a + kL2AStage;
+                    if (rank == 0) mbar_arrive_expect_tx(full + 8 * s, 2 * kL2StageBytes);  // both CTAs' bytes
+                    tma_load_2d_pair(a, &tmH, kc * kLmK, static_cast<int>(row0), full + 8 * s);
+                    tma_load_2d_pair(b, &tmW, kc * kLmK, (nbeg + n) * kLmN + 128 * static_cast<int>(rank), full + 8 * s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0 && lane == 0) {  // MMA issuer (leader CTA only)
+            uint32_t it = 0;
+            for (int n = 0; n < ntiles; ++n) {
+                const uint32_t buf = n & 1;
+                if (n >= 2) mbar_wait(acc_empty + 8 * buf, ((n >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + buf * kLmN;
+                for (int kc = 0; kc < nk; ++kc, ++it) {
+                    const uint32_t s = it % kL2Stages;
+                    mbar_wait(full + 8 * s, (it / kL2Stages) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a = sbase + s * kL2StageBytes, b = a + kL2AStage;
+#pragma unroll
+                    for (int k = 0; k < kLmK / 16; ++k)
+                        umma_f16_pair(d, smem_desc_sw128(a + 32 * k), smem_desc_sw128(b + 32 * k), kL2Idesc,
+                                      (kc > 0 || k > 0) ? 1u : 0u);
+                    umma_commit_pair(empty + 8 * s);
+                }
+                umma_commit_pair(acc_full + 8 * buf);
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const int64_t row = row0 + 32 * q + lane;
+        const int32_t tk = row < T ? tok[row] : -1;
+        const float L = 1.4426950408889634f;
+        float m = -CUDART_INF_F, ssum = 0.0f, xt = 0.0f;
+        const uint32_t acc_empty_leader = mapa(acc_empty, 0);
+        for (int n = 0; n < ntiles; ++n) {
+            const uint32_t buf = n & 1;
+            mbar_wait_sleep(acc_full + 8 * buf, (n >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kLmN;
+#pragma unroll 1
+            for (int c = 0; c < kLmN; c += 32) {
+                float v[32];
+                tmem_ld32(taddr + c, v);
+                const int col0 = (nbeg + n) * kLmN + c;
+                float cm = -CUDART_INF_F;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (col0 + i < V) cm = fmaxf(cm, v[i]);
+                const float mn = fmaxf(m, cm);
+                float acc = 0.0f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (col0 + i < V) acc += ex2_approx((v[i] - mn) * L);
+                ssum = (m == -CUDART_INF_F ? 0.0f : ssum * ex2_approx((m - mn) * L)) + acc;
+                m = mn;
+                if (tk >= col0 && tk < col0 + 32) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (tk == col0 + i) xt = v[i];
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                 acc_empty_leader + 8 * buf)
+                             : "memory");
+        }
+        if (row < T) {
+            pm[static_cast<int64_t>(split) * T + row] = m;
+            ps[static_cast<int64_t>(split) * T + row] = ssum;
+            if (tk >= nbeg * kLmN && tk < (nbeg + ntiles) * kLmN) xtok[row] = xt;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
 namespace {
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -348,9 +526,34 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
     e = cudaMallocAsync(&part, static_cast<size_t>(2) * nsplit * T * sizeof(float), st);
     if (e != cudaSuccess) return e;
     const int group = lm_group(nblk, K);
+    const char* two = std::getenv("RF_LMHEAD_2CTA");  // default on; "0" selects the one-CTA kernel
+    if (!(two && two[0] == '0')) {
+        CUtensorMap mw2;
+        if (!make_map(&mw2, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), 128)) return cudaErrorInvalidValue;
+        e = cudaFuncSetAttribute(lmhead2_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kL2Smem));
+        if (e != cudaSuccess) return e;
+        const int64_t npair = (T + 255) / 256;
+        const int group2 = std::max(1, lm_group(npair, K) / 2);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(2 * npair * nsplit));
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = kL2Smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, lmhead2_stats_kernel, mh, mw2, tok, T, V, K, tps, part,
+                               part + static_cast<size_t>(nsplit) * T, xtok, nsplit, group2);
+    } else {
     lmhead_kernel<0><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
         mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok, nullptr, nullptr, nullptr, 0,
         nsplit, group);
+    }
     lmhead_combine_kernel<<<static_cast<unsigned>((T + 255) / 256), 256, 0, st>>>(
         part, part + static_cast<size_t>(nsplit) * T, nsplit, T, lse);
     e = cudaGetLastError();
