@@ -85,6 +85,39 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// dlogits of one 32-column chunk of a token row: k·(1[v = tok] − exp(x − lse)), bf16
+__device__ __forceinline__ void dl_store_chunk(__nv_bfloat16* drow, const float* v, int col0, int V, int tk, float negk,
+                                               double kd, float lseL, float lse, bool st256) {
+    constexpr float L = 1.4426950408889634f;
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        float o0 = negk * ex2_approx(fmaf(v[2 * i], L, -lseL));
+        float o1 = negk * ex2_approx(fmaf(v[2 * i + 1], L, -lseL));
+        if (kd == 0.0) o0 = o1 = 0.0f;
+        if (tk == col0 + 2 * i) o0 = static_cast<float>(kd - kd * exp(static_cast<double>(v[2 * i]) - lse));
+        if (tk == col0 + 2 * i + 1) o1 = static_cast<float>(kd - kd * exp(static_cast<double>(v[2 * i + 1]) - lse));
+        w[i] = pack_bf16x2(o0, o1);
+    }
+    if (col0 + 32 <= V) {
+        if (st256) {  // two full 32-byte sectors per thread (STG.256)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(drow + col0 + 16 * i),
+                             "r"(w[8 * i]), "r"(w[8 * i + 1]), "r"(w[8 * i + 2]), "r"(w[8 * i + 3]), "r"(w[8 * i + 4]),
+                             "r"(w[8 * i + 5]), "r"(w[8 * i + 6]), "r"(w[8 * i + 7])
+                             : "memory");
+        } else {
+            uint4* d4 = reinterpret_cast<uint4*>(drow + col0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        }
+    } else {
+        for (int i = 0; i < 32 && col0 + i < V; ++i)
+            drow[col0 + i] = __ushort_as_bfloat16(static_cast<uint16_t>((i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xffffu)));
+    }
+}
+
 }  // namespace
 
 // Grouped raster over (128-token block, vocab split): panels of `group` token blocks; inside a
@@ -208,36 +241,7 @@ __global__ void __launch_bounds__(192, 1)
                 const int col0 = (nbeg + n) * kLmN + c;
                 if constexpr (MODE == 1) {
                     if (drow == nullptr) continue;
-                    uint32_t w[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float o0 = negk * ex2_approx(fmaf(v[2 * i], L, -lseL));
-                        float o1 = negk * ex2_approx(fmaf(v[2 * i + 1], L, -lseL));
-                        if (kd == 0.0) o0 = o1 = 0.0f;
-                        if (tk == col0 + 2 * i) o0 = static_cast<float>(kd - kd * exp(static_cast<double>(v[2 * i]) - lse_in[row]));
-                        if (tk == col0 + 2 * i + 1)
-                            o1 = static_cast<float>(kd - kd * exp(static_cast<double>(v[2 * i + 1]) - lse_in[row]));
-                        w[i] = pack_bf16x2(o0, o1);
-                    }
-                    if (col0 + 32 <= V) {
-                        if (st256) {  // two full 32-byte sectors per thread (STG.256)
-#pragma unroll
-                            for (int i = 0; i < 2; ++i)
-                                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(
-                                                 drow + col0 + 16 * i),
-                                             "r"(w[8 * i]), "r"(w[8 * i + 1]), "r"(w[8 * i + 2]), "r"(w[8 * i + 3]),
-                                             "r"(w[8 * i + 4]), "r"(w[8 * i + 5]), "r"(w[8 * i + 6]), "r"(w[8 * i + 7])
-                                             : "memory");
-                        } else {
-                            uint4* d4 = reinterpret_cast<uint4*>(drow + col0);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                d4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-                        }
-                    } else {
-                        for (int i = 0; i < 32 && col0 + i < V; ++i)
-                            drow[col0 + i] = __ushort_as_bfloat16(static_cast<uint16_t>((i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xffffu)));
-                    }
+                    dl_store_chunk(drow, v, col0, V, tk, negk, kd, lseL, lse_in[row], st256);
                     continue;
                 }
                 float cm = -CUDART_INF_F;
@@ -312,11 +316,13 @@ __device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
 }
 }  // namespace
 
+template <int MODE>
 __global__ void __launch_bounds__(192, 1)
-    lmhead2_stats_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
-                         const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
-                         float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok, int32_t nsplit,
-                         int32_t group) {
+    lmhead2_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
+                   const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
+                   float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok, int32_t nsplit,
+                   int32_t group, const float* __restrict__ lse_in, const double* __restrict__ coef,
+                   __nv_bfloat16* __restrict__ dl, int64_t dl_stride) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -404,6 +410,11 @@ __global__ void __launch_bounds__(192, 1)
         const float L = 1.4426950408889634f;
         float m = -CUDART_INF_F, ssum = 0.0f, xt = 0.0f;
         const uint32_t acc_empty_leader = mapa(acc_empty, 0);
+        const float lseL = (MODE == 1 && row < T) ? lse_in[row] * L : 0.0f;
+        const double kd = (MODE == 1 && row < T) ? coef[row] : 0.0;
+        const float negk = static_cast<float>(-kd);
+        __nv_bfloat16* drow = (MODE == 1 && row < T) ? dl + row * dl_stride : nullptr;
+        const bool st256 = MODE == 1 && (dl_stride * 2) % 32 == 0 && (reinterpret_cast<uintptr_t>(dl) & 31) == 0;
         for (int n = 0; n < ntiles; ++n) {
             const uint32_t buf = n & 1;
             mbar_wait_sleep(acc_full + 8 * buf, (n >> 1) & 1);
@@ -414,6 +425,11 @@ __global__ void __launch_bounds__(192, 1)
                 float v[32];
                 tmem_ld32(taddr + c, v);
                 const int col0 = (nbeg + n) * kLmN + c;
+                if constexpr (MODE == 1) {
+                    if (drow == nullptr) continue;
+                    dl_store_chunk(drow, v, col0, V, tk, negk, kd, lseL, lse_in[row], st256);
+                    continue;
+                }
                 float cm = -CUDART_INF_F;
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
@@ -438,7 +454,7 @@ __global__ void __launch_bounds__(192, 1)
                                  acc_empty_leader + 8 * buf)
                              : "memory");
         }
-        if (row < T) {
+        if (MODE == 0 && row < T) {
             pm[static_cast<int64_t>(split) * T + row] = m;
             ps[static_cast<int64_t>(split) * T + row] = ssum;
             if (tk >= nbeg * kLmN && tk < (nbeg + ntiles) * kLmN) xtok[row] = xt;
@@ -530,7 +546,7 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
     if (!(two && two[0] == '0')) {
         CUtensorMap mw2;
         if (!make_map(&mw2, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), 128)) return cudaErrorInvalidValue;
-        e = cudaFuncSetAttribute(lmhead2_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(lmhead2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kL2Smem));
         if (e != cudaSuccess) return e;
         const int64_t npair = (T + 255) / 256;
@@ -547,8 +563,10 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, lmhead2_stats_kernel, mh, mw2, tok, T, V, K, tps, part,
-                               part + static_cast<size_t>(nsplit) * T, xtok, nsplit, group2);
+        e = cudaLaunchKernelEx(&cfg, lmhead2_kernel<0>, mh, mw2, tok, T, V, K, tps, part,
+                               part + static_cast<size_t>(nsplit) * T, xtok, nsplit, group2,
+                               static_cast<const float*>(nullptr), static_cast<const double*>(nullptr),
+                               static_cast<__nv_bfloat16*>(nullptr), static_cast<int64_t>(0));
     } else {
     lmhead_kernel<0><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
         mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok, nullptr, nullptr, nullptr, 0,
@@ -580,6 +598,31 @@ cudaError_t launch_lmhead_dlogits(const void* H, const void* W, const int32_t* t
     const int tps = (ntiles + nsplit - 1) / nsplit;
     nsplit = (ntiles + tps - 1) / tps;
     const int group = lm_group(nblk, K);
+    const char* two = std::getenv("RF_LMHEAD_2CTA");  // default on; "0" selects the one-CTA kernel
+    if (!(two && two[0] == '0')) {
+        CUtensorMap mw2;
+        if (!make_map(&mw2, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), 128)) return cudaErrorInvalidValue;
+        e = cudaFuncSetAttribute(lmhead2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kL2Smem));
+        if (e != cudaSuccess) return e;
+        const int64_t npair = (T + 255) / 256;
+        const int group2 = std::max(1, lm_group(npair, K) / 2);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(2 * npair * nsplit));
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = kL2Smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, lmhead2_kernel<1>, mh, mw2, tok, T, V, K, tps, static_cast<float*>(nullptr),
+                                  static_cast<float*>(nullptr), static_cast<float*>(nullptr), nsplit, group2, lse,
+                                  coef, static_cast<__nv_bfloat16*>(dlogits), dl_stride);
+    }
     lmhead_kernel<1><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
         mh, mw, tok, T, V, K, tps, nullptr, nullptr, nullptr, lse, coef, static_cast<__nv_bfloat16*>(dlogits),
         dl_stride, nsplit, group);
