@@ -60,14 +60,16 @@ def lmhead_dlogits(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch
     return out[:, :V]
 
 
-def lmhead_loss_and_grad(config, hidden: torch.Tensor, w_vocab: torch.Tensor, batch, stream=None):
+def lmhead_loss_and_grad(config, hidden: torch.Tensor, w_vocab: torch.Tensor, batch, stream=None,
+                         check: bool = True):
     """The off-policy loss and dlogits from hidden states, logits never materialised:
     tensor-core stats sweep (lse, sampled logit) -> per-token loss math
     (``rf_token_loss_from_stats``, reference semantics) -> tensor-core dlogits sweep.
 
     ``batch`` is a ``losses.PackedBatch`` whose ``logits`` is only a placeholder
     (``vocab`` must be set); token_mean aggregation, no exact KL.  Returns a
-    ``losses.LossResult`` (dlogits bf16 [T, V])."""
+    ``losses.LossResult`` (dlogits bf16 [T, V]).  ``check=False`` skips the final
+    synchronisation and status check (stream-ordered use)."""
     import ctypes
 
     from . import losses as L
@@ -98,9 +100,10 @@ def lmhead_loss_and_grad(config, hidden: torch.Tensor, w_vocab: torch.Tensor, ba
     if st != 0:
         raise L.InvalidArgument(L.status_string(st))
     dl = lmhead_dlogits(hidden, w_vocab, batch.token_ids, lse, out["coef"], stream)
-    torch.cuda.synchronize(dev)
-    dst = int(status.item())
-    if dst & _abi.RF_DEVSTAT_NONFINITE_RATIO:
-        raise L.InvalidArgument(L.status_string(_abi.RF_ERR_NONFINITE_RATIO))
+    if check:  # synchronises, then raises like the reference (losses.cpp:267)
+        torch.cuda.synchronize(dev)
+        dst = int(status.item())
+        if dst & _abi.RF_DEVSTAT_NONFINITE_RATIO:
+            raise L.InvalidArgument(L.status_string(_abi.RF_ERR_NONFINITE_RATIO))
     return L.LossResult(scalars=scalars, dlogits=dl, token_logp=out["lp"], token_ratio=out["ratio"],
                         token_coef=out["coef"], token_loss=out["loss"], token_flags=flags)
