@@ -311,10 +311,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     Mc = static_cast<double>(Mx);
                     Myc = static_cast<double>(Myx);
                 }
+                // the gradient needs lse, k and D only: publish them first; the reference lse
+                // and the KL value (loss and scalars only) follow off the critical path
                 const double lse = kLn2 * (Mc + log2(Sc));
-                const double lseq = kLn2 * (Myc + log2(Syc));
-                const double D = Tc / Sc;           // Σ p_v (x_v - y_v)
-                const double klv = D - lse + lseq;  // Σ p_v (lp_v - lq_v)
+                const double D = Tc / Sc;  // Σ p_v (x_v - y_v)
                 TokenResult tr;
                 double lp = CUDART_NAN;
                 if (!tok_ok) {
@@ -329,8 +329,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     if (tr.flags & RF_FLAG_NONFINITE) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
                 }
                 const double ks = pre.scale;
-                const double kl_scaled = __dmul_rn(ks, klv);
-                tr.loss = tr.loss - __dmul_rn(__dmul_rn(ks, p.kl_weight), klv);
                 const double kc = -p.grad_sign * ks * p.kl_weight;
                 const float lseL = static_cast<float>(lse * 1.4426950408889634);
                 bc->k = tr.k;
@@ -347,6 +345,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     bc->tok = -1;
                 }
                 mbar_arrive(bar_bc + 8 * par);
+                const double lseq = kLn2 * (Myc + log2(Syc));
+                const double klv = D - lse + lseq;  // Σ p_v (lp_v - lq_v)
+                const double kl_scaled = __dmul_rn(ks, klv);
+                tr.loss = tr.loss - __dmul_rn(__dmul_rn(ks, p.kl_weight), klv);
                 if (rank == 0) {
                     if (p.token_logp) p.token_logp[t] = lp;
                     if (p.token_ratio) p.token_ratio[t] = tr.ratio;
