@@ -8,7 +8,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "rf_kernels.h"
@@ -196,6 +198,17 @@ int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t s
     return n;
 }
 
+// exact KL: CTA groups exchanging through L2 (rf_ring_kl.cu GX) fill all 148 SMs
+// where 4-CTA hardware clusters place on 132; RF_KL_GX=0 selects the clusters (A/B).
+constexpr int kKlMaxGroups = 256;
+bool kl_groups_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("RF_KL_GX");
+        return e && std::string(e) == "1";
+    }();
+    return on;
+}
+
 int generic_grid(int64_t T) { return static_cast<int>(std::min<int64_t>(T, rf::kGenericMaxGrid)); }
 
 int64_t partial_rows(const rf_batch* b) {
@@ -205,6 +218,7 @@ int64_t partial_rows(const rf_batch* b) {
 struct WsLayout {
     double* partials = nullptr;
     double *lse = nullptr, *lp = nullptr, *coef = nullptr, *klx = nullptr, *lseq = nullptr;
+    void* xch = nullptr;  // exact-KL CTA-group exchange slots
     size_t bytes = 0;
 };
 
@@ -218,6 +232,7 @@ WsLayout ws_layout(const rf_loss_config* c, const rf_batch* b, void* base) {
         return static_cast<double*>(r);
     };
     w.partials = take(static_cast<size_t>(partial_rows(b)) * RF_NUM_SCALARS * sizeof(double));
+    if (c->variant == RF_GRPO && c->kl_weight > 0.0) w.xch = take(kKlMaxGroups * 32 * 40);
     if (c->aggregation == RF_SEQUENCE_PRODUCT) {
         const size_t T = static_cast<size_t>(b->num_tokens);
         w.lse = take(T * 8);
@@ -231,6 +246,16 @@ WsLayout ws_layout(const rf_loss_config* c, const rf_batch* b, void* base) {
 }
 
 rf_status check_cuda(cudaError_t e) { return e == cudaSuccess ? RF_OK : RF_ERR_CUDA; }
+
+// sequence_product stats pass: the read-only online-softmax stream (K2st) by default;
+// RF_SP_STATS=ring selects the lag kernel in stats mode (A/B).
+static bool sp_stats_on_ring() {
+    static const bool ring = [] {
+        const char* e = std::getenv("RF_SP_STATS");
+        return e && std::string(e) == "ring";
+    }();
+    return ring;
+}
 
 // Per-phase cycle counters of the lag kernel (profiling aid): enabled by the
 // environment variable RF_DEBUG_COUNTERS=1, read with rf_debug_counters().
@@ -463,10 +488,14 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.row_vecs = g.row_vecs;
             p.nchunks = g.nchunks;
             p.nslots = g.nslots;
-            const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
-            const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-            if (rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s) != cudaSuccess)
+            if (sp_stats_on_ring()) {  // A/B arm: the lag kernel in stats mode
+                const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
+                const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
+                if (rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s) != cudaSuccess)
+                    return RF_ERR_CUDA;
+            } else if (rf::launch_stream_stats(p, ib, s) != cudaSuccess) {
                 return RF_ERR_CUDA;
+            }
         } else {
             if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
         }
@@ -495,7 +524,17 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.row_vecs = g.row_vecs;
             p.nchunks = g.nchunks;
             p.nslots = g.nslots;
-            const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
+            int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
+            if (g.kind == 3 && g.cs > 1 && kl_groups_enabled()) {
+                static std::atomic<unsigned long long> epoch{0};
+                int dev = 0, sms = 148;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                maxc = std::min(kKlMaxGroups, sms / g.cs);
+                p.vcs = g.cs;
+                p.xch = ws.xch;
+                p.xch_epoch = ++epoch;
+            }
             const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
             const cudaError_t e = g.kind == 3   ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
                                   : g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s)

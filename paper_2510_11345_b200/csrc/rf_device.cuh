@@ -59,6 +59,10 @@ struct KParams {
     int32_t nslots;       // ring slots
     int32_t mode;         // 0 = fused loss+dlogits, 1 = stats only (lse/lp), 2 = write with known lse/coef
     unsigned long long* dbg;  // optional per-phase cycle counters (RF_DEBUG_COUNTERS), else nullptr
+    // exact-KL kernel with CTA groups exchanging through L2 instead of a hardware cluster
+    void* xch;                 // [groups][4 row slots][8 ranks] exchange slots (workspace)
+    unsigned long long xch_epoch;  // launch epoch in the high half of the slot sequence words
+    int32_t vcs;               // CTAs per group (0 = hardware cluster)
 };
 
 // Per-phase cycle counters are compiled in only for the profiling build
@@ -260,6 +264,32 @@ __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
     asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
     return v;
 }
+// gpu-scope exchange through L2 (CTA groups without a hardware cluster)
+__device__ __forceinline__ void st_relaxed_gpu_f64(double* a, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu_f32(float* a, float v) {
+    asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_relaxed_gpu_f64(const double* a) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_relaxed_gpu_f32(const float* a) {
+    float v;
+    asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(a) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

@@ -255,16 +255,14 @@ __global__ void __launch_bounds__(NT) generic_kernel(const __grid_constant__ KPa
 }
 
 // ===========================================================================
-// K2s: sequence_product per-sequence scalars (losses.cpp:180-259).  One thread
-// per sequence of this call; token order sums exactly as the reference.
+// K2s: sequence_product per-sequence scalars (losses.cpp:180-259).  One warp
+// per sequence of this call; deterministic warp-tree sums.
 // Writes per-token coef/flags/loss/ratio and a per-sequence partial row.
 // ===========================================================================
 __global__ void seq_kernel(const __grid_constant__ KParams p, int64_t seq_begin, int64_t nseq,
                            double* __restrict__ coef_out) {
-    // One warp per sequence.  The trajectory sums keep the reference's token order
-    // (lanes load 32 tokens at a time, every lane adds them in order from shuffles,
-    // so every lane holds the exact sequential sums); the per-token outputs are
-    // written by all lanes in parallel.
+    // One warp per sequence: the trajectory sums as a warp reduction, the per-token
+    // outputs written by all lanes in parallel.
     const int lane = threadIdx.x & 31;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= nseq) return;  // whole warps
@@ -275,23 +273,33 @@ __global__ void seq_kernel(const __grid_constant__ KParams p, int64_t seq_begin,
     const bool kl = (p.variant == RF_GRPO) && (p.kl_weight > 0.0);
     const bool dppo = p.variant == RF_DECOUPLED_PPO;
     const bool cap = p.mismatch_cap > 0.0;
+    // Lane-strided partial sums, then a fixed shuffle tree with lane 0's result
+    // broadcast: deterministic, identical on every lane.  The per-token lp the sums
+    // read already differ from the reference's in the last bits (fp32 softmax sums),
+    // so the reference's strictly sequential order (losses.cpp:187-252) would buy no
+    // exactness; it cost a 4-deep fp64 dependency chain per token (0.47 ms per
+    // 65K-token chunk on 8K-token sequences).
     double LR = 0.0, logp_sum = 0.0, LPX = 0.0, LM = 0.0;
-    for (int64_t tb = t0; tb < t1; tb += 32) {
-        const int64_t t = tb + lane;
-        const bool ok = t < t1;
-        const double lp = ok ? p.token_logp[t] : 0.0;
-        const double b = ok ? load_logp(p.behavior_logp, t, p.logp_f64) : 0.0;
-        const double dlr = __dsub_rn(lp, b);
-        const double dpx = (dppo && ok) ? __dsub_rn(lp, load_logp(p.prox_logp, t, p.logp_f64)) : 0.0;
-        const double dm = (cap && ok) ? __dsub_rn(b, load_logp(p.engine_logp, t, p.logp_f64)) : 0.0;
-        const int n = static_cast<int>((t1 - tb) < 32 ? (t1 - tb) : 32);
-        for (int k = 0; k < n; ++k) {  // token order (losses.cpp:187-252)
-            LR = __dadd_rn(LR, __shfl_sync(0xffffffffu, dlr, k));
-            logp_sum = __dadd_rn(logp_sum, __shfl_sync(0xffffffffu, lp, k));
-            if (dppo) LPX = __dadd_rn(LPX, __shfl_sync(0xffffffffu, dpx, k));
-            if (cap) LM = __dadd_rn(LM, __shfl_sync(0xffffffffu, dm, k));
-        }
+#pragma unroll 4
+    for (int64_t t = t0 + lane; t < t1; t += 32) {
+        const double lp = p.token_logp[t];
+        const double b = load_logp(p.behavior_logp, t, p.logp_f64);
+        LR += __dsub_rn(lp, b);
+        logp_sum += lp;
+        if (dppo) LPX += __dsub_rn(lp, load_logp(p.prox_logp, t, p.logp_f64));
+        if (cap) LM += __dsub_rn(b, load_logp(p.engine_logp, t, p.logp_f64));
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        LR += __shfl_down_sync(0xffffffffu, LR, o);
+        logp_sum += __shfl_down_sync(0xffffffffu, logp_sum, o);
+        LPX += __shfl_down_sync(0xffffffffu, LPX, o);
+        LM += __shfl_down_sync(0xffffffffu, LM, o);
+    }
+    LR = __shfl_sync(0xffffffffu, LR, 0);
+    logp_sum = __shfl_sync(0xffffffffu, logp_sum, 0);
+    LPX = __shfl_sync(0xffffffffu, LPX, 0);
+    LM = __shfl_sync(0xffffffffu, LM, 0);
     uint32_t flags = 0;
     const double em = exp(LM);
     const double m = cap ? ((p.mismatch_cap < em) ? p.mismatch_cap : em) : 1.0;

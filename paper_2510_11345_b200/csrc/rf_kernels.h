@@ -72,6 +72,8 @@ cudaError_t ring_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int
 cudaError_t launch_generic(const KParams& p, bool in_bf16, bool out_bf16, int grid, cudaStream_t st);
 // K2w (rf_stream.cu): dlogits from per-token coef + lse (needs p.row_vecs, ring-compatible layout)
 cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st);
+// K2st (rf_stream.cu): stats pass of sequence_product (lse, lp per token), read-only online softmax
+cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st);
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st);
 cudaError_t launch_token_loss(const KParams& p, const float* lse, const float* xtok, cudaStream_t st);
 cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, cudaStream_t st);

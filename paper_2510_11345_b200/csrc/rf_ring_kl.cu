@@ -124,7 +124,17 @@ __device__ __forceinline__ float vmax_row(const uint4* r, int n) {
 
 }  // namespace
 
-template <bool OUT_BF16, int NCW, int NVT>
+// GX: the row's CTAs form a GROUP of p.vcs consecutive blocks of a cooperative
+// (all-resident) launch instead of a hardware cluster, and exchange their partials
+// through L2.  4-CTA clusters of one-SM CTAs place only 33 clusters (132 of 148
+// SMs); 37 groups of 4 use every SM.
+struct XSlotG {  // [group][row % 4][sender rank]
+    double S, T, Sy;
+    float M, My;
+    unsigned long long seq;  // (launch epoch << 32) | (row_iter + 1)
+};
+
+template <bool OUT_BF16, int NCW, int NVT, bool GX>
 __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid_constant__ KParams p) {
     constexpr int NCT = NCW * 32;
     constexpr int EPV = 8;  // bf16 logits
@@ -169,10 +179,11 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const uint32_t rank = cluster_ctarank();
-    const uint32_t csize = cluster_nctarank();
-    const uint32_t cid = cluster_id_x();
-    const uint32_t ncl = ncluster_x();
+    const uint32_t rank = GX ? blockIdx.x % static_cast<uint32_t>(p.vcs) : cluster_ctarank();
+    const uint32_t csize = GX ? static_cast<uint32_t>(p.vcs) : cluster_nctarank();
+    const uint32_t cid = GX ? blockIdx.x / static_cast<uint32_t>(p.vcs) : cluster_id_x();
+    const uint32_t ncl = GX ? gridDim.x / static_cast<uint32_t>(p.vcs) : ncluster_x();
+    XSlotG* xg = GX ? static_cast<XSlotG*>(p.xch) + static_cast<size_t>(cid) * 32 : nullptr;
 
     if (tid == 0) {
         for (int s = 0; s < nslots; ++s) {
@@ -188,7 +199,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
     tmem_fence_before();
-    cluster_sync_all();
+    if (GX)
+        __syncthreads();
+    else
+        cluster_sync_all();
     tmem_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -267,7 +281,48 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     if (syw != 0.0) Syw += syw * combine_factor(redMy[par * NCW + w], Myw);
                 }
                 double Mc = static_cast<double>(Mw), Myc = static_cast<double>(Myw), Sc = Sw, Tc = Tw, Syc = Syw;
-                if (csize > 1) {
+                if (GX && csize > 1) {
+                    const uint32_t xs = row_iter & 3;
+                    XSlotG* mine = xg + xs * 8 + rank;
+                    st_relaxed_gpu_f64(&mine->S, Sw);
+                    st_relaxed_gpu_f64(&mine->T, Tw);
+                    st_relaxed_gpu_f64(&mine->Sy, Syw);
+                    st_relaxed_gpu_f32(&mine->M, Mw);
+                    st_relaxed_gpu_f32(&mine->My, Myw);
+                    const unsigned long long want = (p.xch_epoch << 32) | (row_iter + 1);
+                    st_release_gpu_u64(&mine->seq, want);
+                    float Mq[8], Myq[8];
+                    double Sq[8], Tq[8], Syq[8];
+                    float Mx = -CUDART_INF_F, Myx = -CUDART_INF_F;
+                    for (uint32_t q = 0; q < csize; ++q) {
+                        if (q == rank) {
+                            Mq[q] = Mw, Myq[q] = Myw, Sq[q] = Sw, Tq[q] = Tw, Syq[q] = Syw;
+                        } else {
+                            XSlotG* o = xg + xs * 8 + q;
+                            while (ld_acquire_gpu_u64(&o->seq) != want) __nanosleep(32);
+                            Mq[q] = ld_relaxed_gpu_f32(&o->M);
+                            Myq[q] = ld_relaxed_gpu_f32(&o->My);
+                            Sq[q] = ld_relaxed_gpu_f64(&o->S);
+                            Tq[q] = ld_relaxed_gpu_f64(&o->T);
+                            Syq[q] = ld_relaxed_gpu_f64(&o->Sy);
+                        }
+                        Mx = fmaxf(Mx, Mq[q]);
+                        Myx = fmaxf(Myx, Myq[q]);
+                    }
+                    Sc = 0.0;
+                    Tc = 0.0;
+                    Syc = 0.0;
+                    for (uint32_t q = 0; q < csize; ++q) {  // rank order: identical on every CTA
+                        if (Sq[q] != 0.0) {
+                            const double f = combine_factor(Mq[q], Mx);
+                            Sc += Sq[q] * f;
+                            Tc += Tq[q] * f;
+                        }
+                        if (Syq[q] != 0.0) Syc += Syq[q] * combine_factor(Myq[q], Myx);
+                    }
+                    Mc = static_cast<double>(Mx);
+                    Myc = static_cast<double>(Myx);
+                } else if (csize > 1) {
                     const uint32_t xs = row_iter & 3;
                     XSlot* mine = &xslot[xs * 8 + rank];
                     // payload to every peer, one cluster fence, then the sequence words
@@ -362,7 +417,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         }
         __syncwarp();
         tmem_fence_before();
-        cluster_sync_all();
+        if (GX)
+            __syncthreads();
+        else
+            cluster_sync_all();
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_C));
@@ -555,7 +613,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
     }
     tmem_fence_before();
     __syncwarp();
-    cluster_sync_all();
+    if (GX)
+        __syncthreads();
+    else
+        cluster_sync_all();
     tmem_fence_after();
     if (warp == 0) tmem_dealloc(tmem_base, 512);
 }
@@ -563,8 +624,27 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
 namespace {
 
 template <bool OB, int NCW, int NVT>
+cudaError_t launch_kl_gx(const KParams& p, int groups, size_t smem, cudaStream_t st) {
+    auto kern = ring_kl_kernel<OB, NCW, NVT, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(groups * p.vcs));
+    cfg.blockDim = dim3((NCW + 4) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every group's CTAs co-resident
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <bool OB, int NCW, int NVT>
 cudaError_t launch_kl_t(const KParams& p, int cs, int nclusters, size_t smem, cudaStream_t st, int* maxc) {
-    auto kern = ring_kl_kernel<OB, NCW, NVT>;
+    if (p.vcs > 0 && !maxc) return launch_kl_gx<OB, NCW, NVT>(p, nclusters, smem, st);
+    auto kern = ring_kl_kernel<OB, NCW, NVT, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

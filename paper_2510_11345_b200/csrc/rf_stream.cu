@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "rf_device.cuh"
@@ -32,12 +33,46 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 }
 
 constexpr int kStreamThreads = 256;
-constexpr int kStreamUnroll = 4;
+
+// vectors in flight per thread: RF_STREAM_UNROLL=4|8 (A/B knob, default 4)
+int stream_unroll() {
+    static const int u = [] {
+        const char* e = std::getenv("RF_STREAM_UNROLL");
+        return (e && std::atoi(e) == 8) ? 8 : 4;
+    }();
+    return u;
+}
+
+// min resident CTAs per SM the register allocation is bounded for: the read-only
+// stats stream wants every slot filled (8 CTAs, 32 registers: 6.1 vs 5.2 TB/s), the
+// write stream its unspilled 68 registers (4 CTAs: 6.1 vs 5.5 TB/s at 8).
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+int stats_minb() {
+    static const int m = env_int("RF_STATS_MINB", 8);
+    return m;
+}
+int stream_minb() {
+    static const int m = env_int("RF_STREAM_MINB", 1);
+    return m;
+}
+
+// persistent grid: every CTA resident (grid = SMs x occupancy)
+template <typename K>
+int resident_grid(K kernel, int64_t T) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kStreamThreads, 0);
+    return static_cast<int>(std::min<int64_t>(T, static_cast<int64_t>(sms) * std::max(occ, 1)));
+}
 
 }  // namespace
 
-template <bool IN_BF16, bool OUT_BF16>
-__global__ void __launch_bounds__(kStreamThreads) stream_write_kernel(const __grid_constant__ KParams p) {
+template <bool IN_BF16, bool OUT_BF16, int kStreamUnroll, int MINB>
+__global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(const __grid_constant__ KParams p) {
     constexpr int EPV = IN_BF16 ? 8 : 4;
     constexpr size_t IES = IN_BF16 ? 2 : 4;
     constexpr size_t OES = OUT_BF16 ? 2 : 4;
@@ -106,20 +141,157 @@ __global__ void __launch_bounds__(kStreamThreads) stream_write_kernel(const __gr
     }
 }
 
-cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = static_cast<int>(std::min<int64_t>(p.T, static_cast<int64_t>(sms) * 8));
-    if (in_bf16 && out_bf16)
-        stream_write_kernel<true, true><<<grid, kStreamThreads, 0, st>>>(p);
-    else if (in_bf16)
-        stream_write_kernel<true, false><<<grid, kStreamThreads, 0, st>>>(p);
-    else if (out_bf16)
-        stream_write_kernel<false, true><<<grid, kStreamThreads, 0, st>>>(p);
-    else
-        stream_write_kernel<false, false><<<grid, kStreamThreads, 0, st>>>(p);
+// K2st: the stats pass of sequence_product as a read-only stream — lse and lp per
+// token (policy.cpp:21-40 log-softmax at the sampled token) with an online
+// softmax, so no row is held on chip.  Each thread keeps (C, S): C = fl(M·log2e) of
+// its running max, S = Σ 2^(x·log2e − C) in fp64 (fp32 per batch of kStreamUnroll
+// vectors, rescaled by ex2 of the exact float offset difference when the max moves).
+// 2·V bytes read per token.
+template <bool IN_BF16, int kStreamUnroll, int MINB>
+__global__ void __launch_bounds__(kStreamThreads, MINB) stream_stats_kernel(const __grid_constant__ KParams p) {
+    constexpr int EPV = IN_BF16 ? 8 : 4;
+    constexpr size_t IES = IN_BF16 ? 2 : 4;
+    constexpr float kL2e = 1.4426950408889634f;
+    constexpr int kWarps = kStreamThreads / 32;
+    __shared__ float sC[2][kWarps];
+    __shared__ double sS[2][kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row_vecs = p.row_vecs;
+    const int tail_vec = row_vecs - 1;
+    const int tail_valid = p.V - tail_vec * EPV;
+    const uint64_t L2 = pk2(kL2e, kL2e);
+    int par = 0;
+    for (int64_t t = blockIdx.x; t < p.T; t += gridDim.x, par ^= 1) {
+        const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.logits) + row * p.row_stride * IES;
+        int32_t tok = 0;
+        float x_tok = 0.0f;
+        if (tid == 0) {  // the sampled logit, loaded while the row streams
+            tok = p.token_ids[t];
+            if (tok >= 0 && tok < p.V) x_tok = load_logit(p.logits, row * p.row_stride + tok, IN_BF16);
+        }
+        float C = -CUDART_INF_F;
+        double S = 0.0;
+        for (int v0 = tid; v0 < row_vecs; v0 += kStreamThreads * kStreamUnroll) {
+            uint4 x[kStreamUnroll];
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) {
+                const int v = v0 + u * kStreamThreads;
+                x[u] = (v < row_vecs) ? ldg_nc_v4(src + static_cast<size_t>(v) * 16) : neg_inf_vec<IN_BF16>();
+                if (v == tail_vec && tail_valid != EPV) mask_tail<IN_BF16>(x[u], tail_valid);
+            }
+            float bm = -CUDART_INF_F;
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) {
+                const uint32_t m = vec_max2<IN_BF16>(x[u]);
+                bm = IN_BF16 ? fmaxf(bm, fmaxf(__uint_as_float(m << 16), __uint_as_float(m & 0xffff0000u)))
+                             : fmaxf(bm, __uint_as_float(m));
+            }
+            if (bm == -CUDART_INF_F) continue;  // fully masked batch
+            const float Cb = bm * kL2e;
+            if (Cb > C) {
+                if (S != 0.0) S *= static_cast<double>(ex2_approx(C - Cb));
+                C = Cb;
+            }
+            const uint64_t negC2 = pk2(-C, -C);
+            uint64_t acc = 0;
+#pragma unroll
+            for (int u = 0; u < kStreamUnroll; ++u) {
+                const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+                if (IN_BF16) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t a = ffma2(bf16x2_to_f32x2(w[q]), L2, negC2);
+                        const uint64_t e = pk2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
+                        acc = (u == 0 && q == 0) ? e : fadd2(acc, e);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; q += 2) {
+                        const uint64_t a = ffma2(pk2(__uint_as_float(w[q]), __uint_as_float(w[q + 1])), L2, negC2);
+                        const uint64_t e = pk2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
+                        acc = (u == 0 && q == 0) ? e : fadd2(acc, e);
+                    }
+                }
+            }
+            S += static_cast<double>(lo2(acc)) + static_cast<double>(hi2(acc));
+        }
+        // warp, then CTA combine (rank order: deterministic)
+        float Cw = C;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) Cw = fmaxf(Cw, __shfl_xor_sync(0xffffffffu, Cw, o));
+        double s = (S != 0.0) ? S * static_cast<double>(ex2_approx(C - Cw)) : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            sC[par][warp] = Cw;
+            sS[par][warp] = s;
+        }
+        __syncthreads();  // double-buffered slots: one barrier per row
+        if (tid == 0) {
+            float Cm = -CUDART_INF_F;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) Cm = fmaxf(Cm, sC[par][w]);
+            double Sc = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w)
+                if (sS[par][w] != 0.0) Sc += sS[par][w] * static_cast<double>(ex2_approx(sC[par][w] - Cm));
+            const double lse = 0.69314718055994530942 * (static_cast<double>(Cm) + log2(Sc));
+            const bool tok_ok = tok >= 0 && tok < p.V;
+            p.tok_lse[t] = lse;
+            p.token_logp[t] = tok_ok ? static_cast<double>(x_tok) - lse : CUDART_NAN;
+            if (!tok_ok) atomicOr(p.status, RF_DEVSTAT_TOKEN_OUT_OF_RANGE);
+        }
+    }
+}
+
+template <int U, int MINB>
+cudaError_t launch_stats_u(const KParams& p, bool in_bf16, cudaStream_t st) {
+    if (in_bf16) {
+        auto k = stream_stats_kernel<true, U, MINB>;
+        k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
+    } else {
+        auto k = stream_stats_kernel<false, U, MINB>;
+        k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
+    }
     return cudaGetLastError();
+}
+
+template <bool IB, bool OB, int U, int MINB>
+void launch_write_t(const KParams& p, cudaStream_t st) {
+    auto k = stream_write_kernel<IB, OB, U, MINB>;
+    k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
+}
+
+template <int U, int MINB>
+cudaError_t launch_write_u(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st) {
+    if (in_bf16 && out_bf16)
+        launch_write_t<true, true, U, MINB>(p, st);
+    else if (in_bf16)
+        launch_write_t<true, false, U, MINB>(p, st);
+    else if (out_bf16)
+        launch_write_t<false, true, U, MINB>(p, st);
+    else
+        launch_write_t<false, false, U, MINB>(p, st);
+    return cudaGetLastError();
+}
+
+// A/B knobs: RF_STREAM_UNROLL (vectors in flight per thread), RF_STATS_MINB and
+// RF_STREAM_MINB (min resident CTAs per SM of the stats / write kernels).
+cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st) {
+    const int mb = stats_minb();
+    if (stream_unroll() == 8) return launch_stats_u<8, 1>(p, in_bf16, st);
+    if (mb == 8) return launch_stats_u<4, 8>(p, in_bf16, st);
+    if (mb == 6) return launch_stats_u<4, 6>(p, in_bf16, st);
+    return launch_stats_u<4, 1>(p, in_bf16, st);
+}
+
+cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st) {
+    const int mb = stream_minb();
+    if (stream_unroll() == 8) return launch_write_u<8, 1>(p, in_bf16, out_bf16, st);
+    if (mb == 8) return launch_write_u<4, 8>(p, in_bf16, out_bf16, st);
+    if (mb == 6) return launch_write_u<4, 6>(p, in_bf16, out_bf16, st);
+    return launch_write_u<4, 1>(p, in_bf16, out_bf16, st);
 }
 
 }  // namespace rf

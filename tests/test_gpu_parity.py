@@ -253,3 +253,20 @@ def test_sequence_product_mapping_b_fast_path():
     gpu = rf.loss_and_grad(cfg, pb, kernel="ring")
     ref = run_oracle(case, cfg, normalization=0)
     compare(case, cfg, gpu, ref)
+
+
+@pytest.mark.parametrize("V,f32", [(4099, False), (32005, True), (151936, False)])
+def test_sequence_product_long_sequences(V, f32):
+    """Sequences spanning many 32-token blocks (K2s prefetch + sequential sums), odd
+    vocabulary tails and f32 logits through the streaming stats pass (K2st)."""
+    case = make_case(27, T_seqs=8, G=4, V=V, max_len=160, mapping="A", round_bf16=not f32, stale=0.01)
+    assert np.diff(case.seq_offsets).max() > 64
+    dt = torch.float32 if f32 else torch.bfloat16
+    if f32:
+        case.logits = case.logits.astype(np.float32).astype(np.float64)
+    for variant in ["tis", "decoupled_ppo"]:
+        cfg = _cfg(variant, aggregation="sequence_product")
+        pb = to_device_batch(case, dtype=dt, normalization=L.Normalization.seq_then_batch)
+        gpu = rf.loss_and_grad(cfg, pb, dlogits_dtype=dt, kernel="ring")
+        ref = run_oracle(case, cfg, normalization=0)
+        compare(case, cfg, gpu, ref, out_dtype=dt)
