@@ -204,7 +204,7 @@ constexpr int kKlMaxGroups = 256;
 bool kl_groups_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("RF_KL_GX");
-        return e && std::string(e) == "1";
+        return !(e && std::string(e) == "0");
     }();
     return on;
 }

@@ -2,12 +2,14 @@
 // (grpo with kl_weight > 0: losses.cpp:118-133 kl_and_grad, used per trajectory at
 // :321-326; per token row here, scaled by the token's normalisation like the
 // generic path).  The policy row x and the reference row y of every token are
-// co-resident: each CTA of a 4-CTA cluster (Qwen3 vocabulary) holds a quarter of
+// co-resident: each CTA of a 4-CTA group (Qwen3 vocabulary) holds a quarter of
 // both rows in registers, so one HBM read of x and y and one HBM write of the
 // dlogits row suffice — 6·V bytes per token.
 //
 // Same lag structure as rf_ring_lag.cu (TMA ring -> registers, previous row parked
-// in TMEM, two scalar warps, DSMEM exchange), extended with the reference row:
+// in TMEM, two scalar warps), extended with the reference row.  The group is a
+// cooperative launch's consecutive CTAs exchanging through L2 (GX, default: all
+// 148 SMs) or a hardware cluster exchanging through DSMEM (RF_KL_GX=0):
 //
 //   sweep:  e_v = 2^(x_v·log2e - C), ey_v = 2^(y_v·log2e - Cy), d_v = x_v - y_v
 //           S = Σ e, Sy = Σ ey, T = Σ e·d         (per thread, then warp, CTA, cluster)
