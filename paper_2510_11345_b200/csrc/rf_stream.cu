@@ -34,6 +34,29 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 
 constexpr int kStreamThreads = 256;
 
+// 2^a for a packed pair on the FMA pipe (offloads the MUFU, which bounds the
+// read-only stats stream: 8 ex2 per 16-byte vector).  Round-to-nearest split
+// a = n + f (magic-number add), degree-5 near-minimax polynomial for 2^f on
+// [-1/2, 1/2] (max relative error 2.3e-7, the ex2.approx class), exponent added
+// as integer bits.  Arguments are clamped at -125 (2^-125 stands in for 0).
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t a) {
+    const float a0 = fmaxf(lo2(a), -125.0f), a1 = fmaxf(hi2(a), -125.0f);
+    const uint64_t x = pk2(a0, a1);
+    const uint64_t j = fadd2(x, pk2(12582912.0f, 12582912.0f));  // 1.5·2^23 + n
+    const uint64_t r = fadd2(j, pk2(-12582912.0f, -12582912.0f)); // n as float
+    const uint64_t fr = ffma2(r, pk2(-1.0f, -1.0f), x);            // f = a - n
+    uint64_t q = ffma2(pk2(0.001327647129073739f, 0.001327647129073739f), fr,
+                       pk2(0.009675540961325169f, 0.009675540961325169f));
+    q = ffma2(q, fr, pk2(0.05550713092088699f, 0.05550713092088699f));
+    q = ffma2(q, fr, pk2(0.24022120237350464f, 0.24022120237350464f));
+    q = ffma2(q, fr, pk2(0.6931469440460205f, 0.6931469440460205f));
+    q = ffma2(q, fr, pk2(1.0000001192092896f, 1.0000001192092896f));
+    // bits(j) << 23 == n << 23 (the magic's own bits vanish mod 2^32)
+    const uint32_t lo = static_cast<uint32_t>(q) + (static_cast<uint32_t>(j) << 23);
+    const uint32_t hi = static_cast<uint32_t>(q >> 32) + (static_cast<uint32_t>(j >> 32) << 23);
+    return static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
+}
+
 // vectors in flight per thread: RF_STREAM_UNROLL=4|8 (A/B knob, default 4)
 int stream_unroll() {
     static const int u = [] {
@@ -54,6 +77,16 @@ int stats_minb() {
     static const int m = env_int("RF_STATS_MINB", 8);
     return m;
 }
+// RF_STATS_POLY=1: one element pair per vector through ex2_poly2 (A/B knob)
+int stats_poly() {
+    static const int m = env_int("RF_STATS_POLY", 0);
+    return m;
+}
+// RF_WRITE_POLY=1: the same split in the write stream (A/B knob)
+int write_poly() {
+    static const int m = env_int("RF_WRITE_POLY", 0);
+    return m;
+}
 int stream_minb() {
     static const int m = env_int("RF_STREAM_MINB", 1);
     return m;
@@ -71,7 +104,7 @@ int resident_grid(K kernel, int64_t T) {
 
 }  // namespace
 
-template <bool IN_BF16, bool OUT_BF16, int kStreamUnroll, int MINB>
+template <bool IN_BF16, bool OUT_BF16, int kStreamUnroll, int MINB, bool POLY = false>
 __global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(const __grid_constant__ KParams p) {
     constexpr int EPV = IN_BF16 ? 8 : 4;
     constexpr size_t IES = IN_BF16 ? 2 : 4;
@@ -112,7 +145,12 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(cons
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t a = ffma2(bf16x2_to_f32x2(w[q]), L2, negC2);
-                        w[q] = pack_f16x2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
+                        if (POLY && q == 3) {
+                            const uint64_t e = ex2_poly2(a);
+                            w[q] = pack_f16x2(lo2(e), hi2(e));
+                        } else {
+                            w[q] = pack_f16x2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
+                        }
                     }
                 } else {
                     const uint64_t a01 = ffma2(pk2(__uint_as_float(w[0]), __uint_as_float(w[1])), L2, negC2);
@@ -147,7 +185,7 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(cons
 // its running max, S = Σ 2^(x·log2e − C) in fp64 (fp32 per batch of kStreamUnroll
 // vectors, rescaled by ex2 of the exact float offset difference when the max moves).
 // 2·V bytes read per token.
-template <bool IN_BF16, int kStreamUnroll, int MINB>
+template <bool IN_BF16, int kStreamUnroll, int MINB, bool POLY = false>
 __global__ void __launch_bounds__(kStreamThreads, MINB) stream_stats_kernel(const __grid_constant__ KParams p) {
     constexpr int EPV = IN_BF16 ? 8 : 4;
     constexpr size_t IES = IN_BF16 ? 2 : 4;
@@ -202,7 +240,8 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_stats_kernel(cons
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t a = ffma2(bf16x2_to_f32x2(w[q]), L2, negC2);
-                        const uint64_t e = pk2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
+                        const uint64_t e = (POLY && q == 3) ? ex2_poly2(a)
+                                                             : pk2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
                         acc = (u == 0 && q == 0) ? e : fadd2(acc, e);
                     }
                 } else {
@@ -280,6 +319,11 @@ cudaError_t launch_write_u(const KParams& p, bool in_bf16, bool out_bf16, cudaSt
 // RF_STREAM_MINB (min resident CTAs per SM of the stats / write kernels).
 cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st) {
     const int mb = stats_minb();
+    if (in_bf16 && stats_poly()) {
+        auto k = stream_stats_kernel<true, 4, 8, true>;
+        k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
+        return cudaGetLastError();
+    }
     if (stream_unroll() == 8) return launch_stats_u<8, 1>(p, in_bf16, st);
     if (mb == 8) return launch_stats_u<4, 8>(p, in_bf16, st);
     if (mb == 6) return launch_stats_u<4, 6>(p, in_bf16, st);
@@ -288,6 +332,11 @@ cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st)
 
 cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st) {
     const int mb = stream_minb();
+    if (in_bf16 && out_bf16 && write_poly()) {
+        auto k = stream_write_kernel<true, true, 4, 1, true>;
+        k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
+        return cudaGetLastError();
+    }
     if (stream_unroll() == 8) return launch_write_u<8, 1>(p, in_bf16, out_bf16, st);
     if (mb == 8) return launch_write_u<4, 8>(p, in_bf16, out_bf16, st);
     if (mb == 6) return launch_write_u<4, 6>(p, in_bf16, out_bf16, st);

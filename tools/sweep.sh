@@ -10,3 +10,4 @@ run c3_topr --workload c3 --variant topr --steps 3 --warmup 2
 run c4 --workload c4 --steps 3 --warmup 2
 run c2_seqprod --workload c2 --aggregation sequence_product --steps 3 --warmup 2
 run c5 --workload c5 --steps 2 --warmup 1 --pool-gb 64
+run c2_kl --workload c2 --kl-weight 0.1 --steps 3 --warmup 2 --pool-gb 40
