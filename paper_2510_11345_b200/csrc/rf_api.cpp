@@ -535,10 +535,19 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
                 p.xch = ws.xch;
                 p.xch_epoch = ++epoch;
             }
-            const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-            const cudaError_t e = g.kind == 3   ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
-                                  : g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s)
-                                                : rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
+            int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
+            cudaError_t e = g.kind == 3   ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
+                            : g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s)
+                                          : rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
+            if (e == cudaErrorCooperativeLaunchTooLarge && p.vcs > 0) {
+                // the CTA groups need every CTA co-resident (e.g. SMs held by an MPS
+                // partition): the hardware-cluster version instead
+                cudaGetLastError();
+                p.vcs = 0;
+                ncl = static_cast<int>(
+                    std::min<int64_t>(b->num_tokens, ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem)));
+                e = rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s);
+            }
             if (e != cudaSuccess) return RF_ERR_CUDA;
             nparts = g.kind >= 2 ? 2 * ncl : ncl;  // lag kernels: one partial row per scalar warp
         } else {
