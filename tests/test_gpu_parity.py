@@ -270,3 +270,55 @@ def test_sequence_product_long_sequences(V, f32):
         gpu = rf.loss_and_grad(cfg, pb, dlogits_dtype=dt, kernel="ring")
         ref = run_oracle(case, cfg, normalization=0)
         compare(case, cfg, gpu, ref, out_dtype=dt)
+
+
+def test_grpo_kl_groups_many_rows():
+    """Exact KL at Qwen3 vocab with several rows per CTA group (the L2 exchange slots
+    wrap, row % 4) and two launches (a new epoch in the sequence words): parity, and
+    the second launch bit-identical to the first."""
+    case = make_case(28, T_seqs=20, G=4, V=151936, max_len=64, mapping="A", stale=0.2, kl=True)
+    assert case.T > 4 * 37
+    cfg = _cfg("grpo", kl_weight=0.1)
+    pb = to_device_batch(case, with_ref=True, normalization=L.Normalization.global_token)
+    gpu = rf.loss_and_grad(cfg, pb, kernel="ring")
+    ref = run_oracle(case, cfg, normalization=1)
+    compare(case, cfg, gpu, ref)
+    again = rf.loss_and_grad(cfg, pb, kernel="ring")
+    assert torch.equal(gpu.dlogits, again.dlogits)
+    assert torch.equal(gpu.scalars, again.scalars)
+
+
+_AB_ARM = r"""
+import sys
+sys.path.insert(0, {root!r})
+import paper_2510_11345_b200 as rf
+from paper_2510_11345_b200 import losses as L
+from tests.cases import config, make_case
+from tests.parity import compare, run_oracle, to_device_batch
+kl = {kl!r}
+case = make_case(29, T_seqs=8, G=4, V=151936, max_len=40, mapping="A", stale=0.1, kl=kl)
+if kl:
+    cfg = config("grpo", engine_mismatch_cap=2.0, kl_weight=0.1)
+    pb = to_device_batch(case, with_ref=True, normalization=L.Normalization.global_token)
+    ref = run_oracle(case, cfg, normalization=1)
+else:
+    cfg = config("tis", engine_mismatch_cap=2.0, aggregation="sequence_product")
+    pb = to_device_batch(case, normalization=L.Normalization.seq_then_batch)
+    ref = run_oracle(case, cfg, normalization=0)
+compare(case, cfg, rf.loss_and_grad(cfg, pb, kernel="ring"), ref)
+print("arm ok")
+"""
+
+
+@pytest.mark.parametrize("env,kl", [({"RF_KL_GX": "0"}, True), ({"RF_SP_STATS": "ring"}, False)])
+def test_ab_arms_parity(env, kl):
+    """The A/B arms behind environment knobs (read once per process, so each runs in a
+    subprocess): hardware-cluster exact KL, lag-kernel stats pass of sequence_product."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _AB_ARM.format(root=root, kl=kl)], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "arm ok" in r.stdout, r.stdout + r.stderr
