@@ -1,28 +1,37 @@
 #!/usr/bin/env python
 """Benchmark: fused off-policy loss + dlogits tokens/s and % HBM roofline on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl ours|reference]
 
-One step = the hot path over one synthetic long-tail rollout batch (BASELINE.json
-configs; default C2 = decoupled PPO, Qwen3 vocab 151,936, 256 prompts x 8
-responses per GPU, max len 8k, async ratio 2):
+One step = the hot path over one synthetic long-tail rollout batch of a
+BASELINE.json config.  Default: C5, the config the metric's 1/2/4/8-GPU sweep is
+quoted on (Qwen3 vocab 151,936, 2048 prompts x 16 responses, max len 32k,
+decoupled PPO, async ratio 2), a FIXED global batch whose whole GRPO groups are
+LPT-sharded over the ranks (strong scaling; ``--scaling weak`` gives every rank
+its own copy-sized shard instead):
   K1 GRPO group advantages -> K2 fused log-softmax/gather + ratio + surrogate +
   bf16 dlogits, streamed in token chunks from a device logits pool (rows indexed
   by row_of_token; pool and dlogits buffers far exceed L2) -> K3 scalar reduce ->
   (N > 1) one NCCL all-reduce of the fp64 loss scalars.
-Whole GRPO groups are LPT-sharded across ranks (weak scaling: each rank owns a
-C2-sized shard of an N x C2 global batch).  Timing: CUDA events on the launching
-stream, barrier + synchronize on both sides, max over ranks.
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  ``--gpus N`` without a torchrun environment re-launches
+itself under torch.distributed.run with N ranks.
+
+After the timed region: ``e2e`` (the C-ABI host-buffer call, every rank at
+once), ``cpu_baseline`` (rank 0, N = 1) and the ``--check K`` leg, which holds
+K sampled token rows of the last timed step (plus every GRPO group's
+advantages) to the fp64 oracle (oracle/check.py) — checkers, never timed.
 
 --impl reference times the reference's own CPU implementation (rlsim::loss_and_grad
 compiled from /root/reference into oracle/_ref, one length-1 trajectory per token)
-on the host cores, rank 0 only.
+on the host cores, rank 0 only; that arm never maps the product library.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,10 +49,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's fixed global batch sharded over N; weak: N copies")
     ap.add_argument("--variant", default=None)
     ap.add_argument("--aggregation", default="token_mean", choices=["token_mean", "sequence_product"])
-    ap.add_argument("--prompts", type=int, default=None, help="prompts per rank (default: the config's)")
+    ap.add_argument("--prompts", type=int, default=None,
+                    help="prompts (global for strong scaling, per rank for weak; default: the config's)")
     ap.add_argument("--chunk-tokens", type=int, default=65536)
     ap.add_argument("--pool-gb", type=float, default=48.0)
     ap.add_argument("--kernel", default="auto", choices=["auto", "ring", "generic"])
@@ -53,6 +65,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-tokens", type=int, default=16384)
     ap.add_argument("--cpu-rows", type=int, default=0, help="reference sample rows (0 = auto)")
+    ap.add_argument("--check", type=int, default=256,
+                    help="oracle parity on this many sampled token rows of the last timed step (0 = off)")
     return ap.parse_args()
 
 
@@ -61,6 +75,24 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_under_torchrun(n: int) -> None:
+    """`python bench.py --gpus N` outside torchrun: re-exec with N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd[2:6])} ...", file=sys.stderr, flush=True)
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def load_peaks():
@@ -114,15 +146,24 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_per_token(vocab: int):
-    """dram read+write bytes per token of the ring kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ring_traffic.json")
+def static_traffic(key: str):
+    """dram read+write bytes per token of the dominant kernel from a committed
+    `ncu --set full` capture (profiles/ring_traffic.json) — a static file value,
+    not measured in this run."""
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "ring_traffic.json")) as f:
             d = json.load(f)
-        return d.get(str(vocab), {}).get("dram_bytes_per_token")
+        e = d.get(key)
+        return None if e is None else (e["dram_bytes_per_token"], e.get("source", ""))
     except Exception:
         return None
+
+
+def make_config(variant: str, aggregation: str = "token_mean", kl_weight: float = 0.0):
+    """rlsim::LossConfig defaults (losses.hpp:28-41) for the named variant."""
+    from paper_2510_11345_b200.losses import LossConfig, LossVariant, RatioAggregation
+
+    return LossConfig(variant=LossVariant[variant], aggregation=RatioAggregation[aggregation], kl_weight=kl_weight)
 
 
 # ---------------------------------------------------------------------------
@@ -140,7 +181,7 @@ def reference_sample(wl, rows, variant, seed=42):
     (bf16 logits as fp64), tokens, advantages, behaviour/prox/engine log-probs."""
     import numpy as np
 
-    from paper_2510_11345_b200 import synth as S
+    from paper_2510_11345_b200 import synth as S  # host-side shapes only (no product library)
 
     rb = S.make_rank_batch(wl, 0, 1, seed)
     rng = np.random.default_rng(seed)
@@ -181,13 +222,12 @@ def prepare_reference(wl, variant, rows):
     return (x, tok, adv, beh, prox_tab)
 
 
-def run_reference_once(prep, variant, threads, reps=1):
+def run_reference_once(prep, cfg, threads, reps=1):
     """Wall seconds of rlsim::loss_and_grad over the prepared rows (oracle/_ref)."""
     import oracle as O
-    from tests.cases import config
 
     x, tok, adv, beh, prox_tab = prep
-    secs, _ = O.ref_bench_mapping_a(config(variant), x, tok, adv, beh, prox_logits=prox_tab, engine_logp=None,
+    secs, _ = O.ref_bench_mapping_a(cfg, x, tok, adv, beh, prox_logits=prox_tab, engine_logp=None,
                                     threads=threads, reps=reps)
     return secs
 
@@ -200,7 +240,7 @@ def default_cpu_rows(wl, threads):
 def cpu_baseline(wl, variant, rows):
     threads = host_threads()
     rows = rows or default_cpu_rows(wl, threads)
-    secs = run_reference_once(prepare_reference(wl, variant, rows), variant, threads)
+    secs = run_reference_once(prepare_reference(wl, variant, rows), make_config(variant), threads)
     return {"value": rows / secs, "unit": "tokens/s", "cores": threads, "kind": "reference",
             "sample": f"{rows} token rows of {wl.name} (V={wl.vocab}, {variant}, mapping A: one length-1 "
                       f"trajectory per token), rlsim::loss_and_grad from oracle/_ref on {threads} host threads "
@@ -214,16 +254,17 @@ def impl_reference(args, wl, variant):
     threads = host_threads()
     rows = args.cpu_rows or default_cpu_rows(wl, threads)
     prep = prepare_reference(wl, variant, rows)
+    cfg = make_config(variant)
     for _ in range(args.warmup):
-        run_reference_once(prep, variant, threads)
-    times = [run_reference_once(prep, variant, threads) for _ in range(args.steps)]
+        run_reference_once(prep, cfg, threads)
+    times = [run_reference_once(prep, cfg, threads) for _ in range(args.steps)]
     mean = sum(times) / len(times)
     value = rows / mean
     sample = (f"{rows} token rows of {wl.name} per step (V={wl.vocab}, {variant}, mapping A), "
               f"rlsim::loss_and_grad from oracle/_ref on {threads} host threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.description, "variant": variant, "vocab": wl.vocab, "sample_rows": rows},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
                              "sample": sample},
@@ -234,28 +275,35 @@ def impl_reference(args, wl, variant):
 # ---------------------------------------------------------------------------
 # Our arm
 # ---------------------------------------------------------------------------
-def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1, chunk=512):
-    """The reference-facing C-ABI call with HOST buffers (rf_loss_and_grad_host):
-    pinned host logits rows in, pinned host dlogits + per-token outputs + scalars
-    out; every H2D/D2H copy is inside the timed region."""
+def e2e_host_api(cfg, dw, tokens, world, steps=3, warmup=1, chunk=512):
+    """The reference-facing C-ABI call with HOST buffers (rf_loss_and_grad_host), on
+    every rank at once: pinned host logits rows in, pinned host dlogits + per-token
+    outputs + scalars out; every H2D/D2H copy is inside the timed region.  Returns the
+    whole-job tokens/s (sum of the ranks' tokens / the slowest rank's step time)."""
     import ctypes
 
     import torch
+    import torch.distributed as dist
 
     from paper_2510_11345_b200 import _abi
     from paper_2510_11345_b200 import losses as L
-    from tests.cases import config
 
-    T = min(tokens, dw.T)
-    # whole sequences
+    V = dw.vocab
+    try:  # bound the pinned host memory (logits + dlogits rows) by the box's free RAM
+        import psutil
+
+        avail = psutil.virtual_memory().available
+        tokens = int(max(512, min(tokens, avail * 0.25 / world / (4 * V))))
+    except Exception:
+        pass
     offs = dw.seq_offsets.cpu()
-    n_seq = int(torch.searchsorted(offs, torch.tensor([T]), right=True)[0]) - 1
+    n_seq = int(torch.searchsorted(offs, torch.tensor([min(tokens, dw.T)]), right=True)[0]) - 1
     n_seq = max(n_seq, 1)
     T = int(offs[n_seq])
-    V = dw.vocab
     rows = dw.row_of_token[:T].long()
     h_logits = torch.empty(T, V, dtype=torch.bfloat16, pin_memory=True)
-    h_logits.copy_(dw.pool[rows].cpu())
+    for r0 in range(0, T, 4096):
+        h_logits[r0:r0 + 4096].copy_(dw.pool[rows[r0:r0 + 4096]].cpu())
     h_dl = torch.empty(T, V, dtype=torch.bfloat16, pin_memory=True)
 
     def pin(t):
@@ -274,7 +322,7 @@ def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1, chunk=512):
     h_flags = torch.empty(T, dtype=torch.uint8, pin_memory=True)
     h_scal = torch.zeros(_abi.RF_NUM_SCALARS, dtype=torch.float64, pin_memory=True)
     h_status = torch.zeros(1, dtype=torch.int32, pin_memory=True)
-    cfg = config(variant).to_c()
+    c = cfg.to_c()
     b = _abi.rf_batch()
     b.num_tokens, b.num_seqs, b.vocab = T, n_seq, V
     b.logits_dtype, b.logits, b.logits_row_stride = _abi.RF_DTYPE_BF16, h_logits.data_ptr(), V
@@ -291,21 +339,112 @@ def e2e_host_api(wl, variant, dw, tokens, steps=3, warmup=1, chunk=512):
     lib = _abi.load_library()
     dev = torch.cuda.current_device()
     for _ in range(warmup):
-        st = lib.rf_loss_and_grad_host(ctypes.byref(cfg), ctypes.byref(b), ctypes.byref(o), dev, chunk)
+        st = lib.rf_loss_and_grad_host(ctypes.byref(c), ctypes.byref(b), ctypes.byref(o), dev, chunk)
         assert st == 0, L.status_string(st)
     ts = []
     for _ in range(steps):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        st = lib.rf_loss_and_grad_host(ctypes.byref(cfg), ctypes.byref(b), ctypes.byref(o), dev, chunk)
+        st = lib.rf_loss_and_grad_host(ctypes.byref(c), ctypes.byref(b), ctypes.byref(o), dev, chunk)
         ts.append(time.perf_counter() - t0)
         assert st == 0, L.status_string(st)
-    t = statistics.median(ts)
+    tt = torch.tensor(ts + [float(T)], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        tsum = tt[-1:].clone()
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        T_all = int(tsum.item())
+    else:
+        T_all = T
+    t = statistics.median(tt[:-1].tolist())
     h2d = T * V * 2 + T * (4 + 4 + 4 * 3) + (n_seq + 1) * 8 + n_seq * 8
     d2h = T * V * 2 + T * (8 * 4 + 1) + _abi.RF_NUM_SCALARS * 8 + 4
-    return {"value": T / t, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "sample": f"first {T} tokens ({n_seq} whole sequences) of this rank's batch per step, "
-                      f"rf_loss_and_grad_host (C ABI, pinned host buffers, {chunk}-token chunks "
-                      f"double-buffered over H2D/compute/D2H streams), median of {steps} wall-clock steps"}
+    return {"value": T_all / t, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d * world),
+            "d2h_bytes_per_step": int(d2h * world),
+            "sample": f"first {T} tokens ({n_seq} whole sequences) of each rank's shard per step on {world} "
+                      f"rank(s) at once, rf_loss_and_grad_host (C ABI, pinned host buffers, {chunk}-token chunks "
+                      f"double-buffered over H2D/compute/D2H streams), median over {steps} steps of the slowest "
+                      f"rank's wall-clock step"}
+
+
+def parity_leg(K, cfg, dw, rb, op, calls, k1_out, ref_pool, rank, world, dev, seqprod):
+    """Checker (not timed): K sampled token rows of the last timed step vs the fp64
+    oracle, and every GRPO group's advantages bit-exact.  Returns the merged stats
+    (max over ranks, ``ok`` = every rank ok)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    from oracle.check import check_sample
+
+    rng = np.random.default_rng(4321 + rank)
+    st, adv_o, deg_o = O.oracle_grpo(dw.rewards.cpu().numpy(), dw.group_offsets.cpu().numpy())
+    k1_ok = st == 0 and np.array_equal(k1_out[0].cpu().numpy(), adv_o) and \
+        np.array_equal(k1_out[1].cpu().numpy(), deg_o)
+    _, t1_last, sub_last, out_t0 = calls[-1]
+    t0_last = calls[-1][0]
+    n_last = t1_last - t0_last
+    offs = dw.seq_offsets.cpu().numpy()
+    if not seqprod:
+        a = rng.choice(n_last, size=min(K // 2, n_last), replace=False) + out_t0
+        bsel = rng.choice(dw.T, size=max(0, K - len(a)), replace=False)
+        toks = np.unique(np.concatenate([a, bsel]).astype(np.int64))
+        sub_offs = np.arange(len(toks) + 1, dtype=np.int64)
+        seq_ids = np.searchsorted(offs, toks, side="right") - 1
+    else:
+        # whole (short) sequences: half from the last call (their dlogits rows are still on the device)
+        lens = np.diff(offs)
+        s_last = np.nonzero((offs[:-1] >= out_t0) & (offs[1:] <= out_t0 + n_last) & (lens <= K // 4))[0]
+        s_any = np.nonzero(lens <= K // 4)[0]
+        pick, tot = [], 0
+        for cand, cap in ((s_last, K // 2), (s_any, K)):
+            for s in rng.permutation(cand):
+                if tot >= cap:
+                    break
+                if int(s) not in pick:
+                    pick.append(int(s))
+                    tot += int(lens[s])
+        pick = sorted(set(pick))
+        toks = np.concatenate([np.arange(offs[s], offs[s + 1]) for s in pick]).astype(np.int64)
+        sub_offs = np.zeros(len(pick) + 1, dtype=np.int64)
+        sub_offs[1:] = np.cumsum(lens[pick])
+        seq_ids = np.array(pick, dtype=np.int64)
+    it = torch.from_numpy(toks).to(dev)
+    rows = dw.row_of_token[it].long()
+    X = dw.pool[rows].double().cpu().numpy()
+    Y = ref_pool[rows].double().cpu().numpy() if ref_pool is not None else None
+    f64 = lambda t: t[it].double().cpu().numpy()
+    gpu = {"lp": f64(op.token_logp), "ratio": f64(op.token_ratio), "coef": f64(op.token_coef),
+           "loss": f64(op.token_loss), "flags": op.token_flags[it].cpu().numpy()}
+    dl = {}
+    for i, t in enumerate(toks):
+        if out_t0 <= t < out_t0 + n_last:
+            dl[i] = op.dlogits[int(t - out_t0)].double().cpu().numpy()
+    stats = check_sample(cfg, logits=X, token_ids=dw.token_ids[it].cpu().numpy(), seq_offsets=sub_offs,
+                         advantages=k1_out[0][torch.from_numpy(seq_ids).to(dev)].cpu().numpy(),
+                         behavior_logp=f64(dw.behavior_logp), prox_logp=f64(dw.prox_logp),
+                         engine_logp=f64(dw.engine_logp), ref_logits=Y, normalization=1,
+                         global_num_seqs=rb.global_seqs, global_num_tokens=rb.global_tokens, gpu=gpu, dl_rows=dl)
+    stats["k1_groups_bit_exact"] = bool(k1_ok)
+    stats["ok"] = bool(stats["ok"] and k1_ok)
+    keys = ["lp_rel", "ratio_rel", "coef_rel", "token_loss_err", "dlogit_unit_err"]
+    cnt = ["tokens", "dlogit_rows", "kink_band_tokens", "flag_mismatch", "flag_mismatch_in_band"]
+    if world > 1:
+        mx = torch.tensor([stats[k] for k in keys] + [0.0 if stats["ok"] else 1.0], dtype=torch.float64, device=dev)
+        sm = torch.tensor([stats[k] for k in cnt] + [len(deg_o)], dtype=torch.float64, device=dev)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        stats.update({k: float(v) for k, v in zip(keys, mx.tolist()[:-1])})
+        stats.update({k: int(v) for k, v in zip(cnt, sm.tolist()[:-1])})
+        stats["ok"] = mx[-1].item() == 0.0
+        stats["k1_groups"] = int(sm[-1].item())
+    else:
+        stats["k1_groups"] = len(deg_o)
+    stats["checker"] = ("oracle/rf_oracle.c (fp64 restatement of losses.cpp:137-331, pinned to oracle/_ref) on "
+                        "sampled rows of the last timed step; tolerances BASELINE.md §5")
+    return stats
 
 
 def impl_ours(args, wl, variant):
@@ -315,16 +454,16 @@ def impl_ours(args, wl, variant):
     import paper_2510_11345_b200 as rf
     from paper_2510_11345_b200 import losses as L
     from paper_2510_11345_b200 import synth as S
-    from tests.cases import config
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    rb = S.make_rank_batch(wl, rank, world, 42, args.prompts)
+    strong = args.scaling == "strong"
+    rb = S.make_rank_batch(wl, rank, world, 42, args.prompts, strong=strong)
     dw = S.DeviceWorkload(rb, wl.vocab, pool_gb=args.pool_gb, device=dev, seed=42 + rank)
-    cfg = config(variant, aggregation=args.aggregation, kl_weight=args.kl_weight)
+    cfg = make_config(variant, args.aggregation, args.kl_weight)
     ref_pool = None
     if args.kl_weight > 0:
         # exact-KL GRPO: a second, independent pool of reference-policy rows (π_ref),
@@ -348,7 +487,8 @@ def impl_ours(args, wl, variant):
     k1_out = (torch.empty_like(pb.rewards), torch.empty(dw.group_offsets.numel() - 1, dtype=torch.uint8, device=dev),
               torch.zeros(1, dtype=torch.int32, device=dev))
     pb.advantages = k1_out[0]
-    if args.aggregation == "sequence_product":
+    seqprod = args.aggregation == "sequence_product"
+    if seqprod:
         # whole sequences per call (the sequence weights need every token's log-prob)
         calls = [(0, t1 - t0, sub, t0) for t0, t1, sub in pb.sequence_chunks(chunk)]
         chunk = max(c[1] for c in calls)
@@ -375,7 +515,7 @@ def impl_ours(args, wl, variant):
         step()
     torch.cuda.synchronize()
     # correctness guard on the benchmark data: device status clean
-    assert int(op.status.item()) == 0, "device status set during warm-up"
+    assert int(op.status.item()) == 0 and int(k1_out[2].item()) == 0, "device status set during warm-up"
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -396,7 +536,7 @@ def impl_ours(args, wl, variant):
         dist.barrier()
     clk = clocks.stop()
     ms_total = start.elapsed_time(stop)
-    # ring-kernel time per step: every chunk's launch pair, averaged over the timed steps
+    # dominant-kernel time per step: every chunk's launch pair, averaged over the timed steps
     for evs in ev:
         for a, b2 in evs:
             kern_ms += a.elapsed_time(b2)
@@ -406,37 +546,46 @@ def impl_ours(args, wl, variant):
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step = float(t_local[0]) / args.steps
-    tokens_global = rb.global_tokens
+    tokens_global = rb.global_tokens if strong else rb.global_tokens
     value = tokens_global / (ms_step / 1e3)
+    step_status = int(op.status.item())
 
     peak, peak_kind = load_peaks()
-    seqprod = args.aggregation == "sequence_product"
-    # token_mean: one read + one write of each row (4V B/token); sequence_product: a
-    # stats read pass + a read/write dlogits pass (6V B/token)
-    bytes_tok = (6 if (seqprod or args.kl_weight > 0) else 4) * wl.vocab  # + the π_ref row read
-    # achieved bandwidth of the dominant kernel: algorithmic bytes / kernel time per step
-    achieved = dw.T * bytes_tok / (kern_ms / 1e3) / 1e9
     kl = args.kl_weight > 0
-    tpt = None if (seqprod or kl) else traffic_per_token(wl.vocab)
+    # token_mean: one read + one write of each row (4V B/token); sequence_product: a
+    # stats read pass + a read/write dlogits pass (6V B/token); exact KL: + the π_ref row read
+    bytes_tok = (6 if (seqprod or kl) else 4) * wl.vocab
+    achieved = dw.T * bytes_tok / (kern_ms / 1e3) / 1e9
+    tkey = ("seqprod" if seqprod else "kl" if kl else "lag") + f"/{wl.vocab}"
+    tr = static_traffic(tkey)
     launch_tokens = calls[0][1] - calls[0][0]
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None if tpt is None else int(tpt * launch_tokens),
+            "frac": round(achieved / peak, 4), "traffic": None if tr is None else int(tr[0] * launch_tokens),
+            "traffic_source": None if tr is None else
+            f"static: dram__bytes_read+write per token from a committed ncu --set full capture ({tr[1]}) x "
+            f"{launch_tokens} tokens per launch; not measured in this run",
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, torch bf16 copy)" if peak_kind == "measured"
             else "fallback 6.65 TB/s (B200_PROFILING.md)",
-            "kernel": ("ring_lag_kernel stats pass + seq_kernel + stream_write_kernel (+K3)" if seqprod
+            "kernel": ("stream_stats_kernel + seq_kernel + stream_write_kernel (+K3)" if seqprod
                        else "ring_kl_kernel (K2kl, incl. its K3 finalize launch)" if kl
                        else "ring_lag_kernel (K2, incl. its K3 finalize launch)"),
             "algorithmic_bytes_per_token": bytes_tok, "tokens_per_launch": launch_tokens,
-            "kernel_ms_per_step": round(kern_ms, 3)}
+            "kernel_ms_per_step": round(kern_ms, 3), "per_rank": True}
 
-    line = None
+    # ---- after the timed region: e2e (all ranks), parity checker, CPU baseline ----
+    e2e = None
+    if not args.no_e2e:
+        try:
+            e2e = e2e_host_api(cfg, dw, args.e2e_tokens if world == 1 else min(args.e2e_tokens, 8192), world)
+        except Exception as exc:  # report, do not hide
+            e2e = {"value": None, "unit": "tokens/s", "error": repr(exc)}
+    parity = None
+    if args.check > 0:
+        try:
+            parity = parity_leg(args.check, cfg, dw, rb, op, calls, k1_out, ref_pool, rank, world, dev, seqprod)
+        except Exception as exc:
+            parity = {"ok": False, "error": repr(exc)}
     if rank == 0:
-        e2e = None
-        if not args.no_e2e:
-            try:
-                e2e = e2e_host_api(wl, variant, dw, args.e2e_tokens)
-            except Exception as exc:  # report, do not hide
-                e2e = {"value": None, "unit": "tokens/s", "error": repr(exc)}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
@@ -445,12 +594,13 @@ def impl_ours(args, wl, variant):
                 cpu = {"value": None, "error": repr(exc)}
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl.description, "variant": variant, "aggregation": args.aggregation,
                        "kl_weight": args.kl_weight, "vocab": wl.vocab,
-                       "prompts_per_gpu": args.prompts or wl.prompts, "group": wl.group, "max_len": wl.max_len,
-                       "async_ratio": wl.alpha, "tokens_per_gpu": dw.T, "tokens_global": tokens_global,
+                       "prompts_global": (args.prompts or wl.prompts) * (1 if strong else world),
+                       "group": wl.group, "max_len": wl.max_len, "async_ratio": wl.alpha,
+                       "tokens_rank0": dw.T, "tokens_global": tokens_global,
                        "chunk_tokens": chunk, "logits_pool_rows": dw.pool_rows,
                        "l2": f"inputs larger than L2: logits pool {dw.pool_rows * wl.vocab * 2 / 1e9:.1f} GB, "
                              f"dlogits chunk buffer {chunk * wl.vocab * 2 / 1e9:.1f} GB (L2 126 MB)",
@@ -460,8 +610,10 @@ def impl_ours(args, wl, variant):
             "roofline": roof,
             "clocks": clk,
             "gpu_launches": int(launches),
+            "device_status": step_status,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -471,6 +623,8 @@ def impl_ours(args, wl, variant):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     from paper_2510_11345_b200 import synth as S
 
     wl = S.WORKLOADS[args.workload]

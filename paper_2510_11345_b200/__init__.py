@@ -3,8 +3,13 @@
 The compute path is ``librf_offpolicy.so`` (hand-written sm_100a CUDA behind
 the C ABI of ``include/rf_offpolicy.h``); this package is the host-side mirror
 of the reference's loss interface (rlsim::loss_and_grad and friends).
+
+Importing the package checks that the library was built (ImportError
+otherwise: there is no CPU fallback) but maps it only on the first call, so a
+process that imports only the workload synthesis (``synth``) — e.g. the
+reference arm of bench.py — never loads the product library.
 """
-from ._abi import load_library  # noqa: F401  (raises ImportError if the .so is missing)
+from ._abi import require_library
 from .losses import (  # noqa: F401
     InvalidArgument,
     LossConfig,
@@ -25,4 +30,4 @@ from .losses import (  # noqa: F401
     to_string,
 )
 
-load_library()
+require_library()

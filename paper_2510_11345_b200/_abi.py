@@ -149,16 +149,21 @@ EXPORTED_SYMBOLS = (
 _lib = None
 
 
-def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load librf_offpolicy.so (raises if it was not built)."""
-    global _lib
-    if _lib is not None:
-        return _lib
+def require_library(path: str = LIB_PATH) -> None:
+    """Raise ImportError if librf_offpolicy.so was not built (no CPU fallback)."""
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build it with `make -C {_HERE}` (or __graft_entry__.build()); "
             "there is no CPU fallback for the off-policy loss path"
         )
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Map librf_offpolicy.so (once per process; raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    require_library(path)
     lib = ctypes.CDLL(path)
     P = ctypes.POINTER
     lib.rf_loss_config_default.argtypes = [P(rf_loss_config)]

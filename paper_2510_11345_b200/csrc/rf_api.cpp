@@ -26,7 +26,7 @@ bool is_aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p
 
 struct RingGeometry {
     bool ok = false;
-    int kind = 2;  // 0 small, 1 large, 2 lag, 3 lag + exact-KL reference row
+    int kind = 2;  // 2 lag (K2), 3 lag + exact-KL reference row (K2kl)
     int cs = 1, ncw = 0, nvt = 0;
     int row_vecs = 0, slice_vecs = 0, nchunks = 0, nslots = 0;
     size_t smem = 0;
@@ -44,24 +44,12 @@ int max_optin_smem() {
     return v;
 }
 
-int sm_smem_bytes() {
-    static int v = -1;
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
-    if (v < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess) v = 0;
-    }
-    return v;
-}
-
 size_t dtype_size(int32_t d) { return d == RF_DTYPE_BF16 ? 2 : (d == RF_DTYPE_F32 ? 4 : 8); }
 
-// The ring kernel needs every logits row (and dlogits row) to start on a 16-byte
-// boundary with its 16-byte-padded length inside the row stride.  The row slice
-// of each CTA lives in registers: pick the smallest cluster whose slice fits
-// kRingThreads x NVT vectors, then the smallest NVT instance.
+// The lag kernel (K2) needs every logits row (and dlogits row) to start on a
+// 16-byte boundary with its 16-byte-padded length inside the row stride.  The row
+// slice of each CTA lives in registers: pick the smallest cluster whose slice fits
+// 12 consumer warps x NVT vectors, then the smallest NVT instance.
 RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
     RingGeometry g;
     const size_t es = dtype_size(b->logits_dtype), os = dtype_size(o->dlogits_dtype);
@@ -72,51 +60,27 @@ RingGeometry ring_geometry(const rf_batch* b, const rf_outputs* o) {
     if (o->dlogits == nullptr || !is_aligned(o->dlogits, 16)) return g;
     if ((o->dlogits_row_stride * static_cast<int64_t>(os)) % 16 != 0) return g;
     if (o->dlogits_row_stride < static_cast<int64_t>(g.row_vecs) * epv) return g;
-    // RF_RING_CONFIG: "lag" (default: TMEM-parked previous row, 1 CTA/SM),
-    // "small" (2 CTAs/SM, register-resident) or "large" (1 CTA/SM, register-resident).
-    const char* env = std::getenv("RF_RING_CONFIG");
     g.kind = 2;
-    if (env && std::strcmp(env, "small") == 0) g.kind = 0;
-    if (env && std::strcmp(env, "large") == 0) g.kind = 1;
-    int lag_ncw = rf::kRingWarpsLag;  // RF_LAG_WARPS=8|12|16 (experiments; 8 and 16 are bf16->bf16 only)
-    if (const char* lw = std::getenv("RF_LAG_WARPS")) lag_ncw = std::atoi(lw);
-    if (lag_ncw != 8 && lag_ncw != 12 && lag_ncw != 16) lag_ncw = rf::kRingWarpsLag;
-    const int ncw = g.kind == 2 ? lag_ncw : (g.kind == 1 ? rf::kRingWarpsLarge : rf::kRingWarpsSmall);
-    const int nct = ncw * 32;
-    int smem_cap = max_optin_smem();
-    if (g.kind == 0) smem_cap = std::min(smem_cap, (sm_smem_bytes() - 2 * 1024) / 2);  // two CTAs per SM
-    const size_t tail = g.kind == 2 ? rf::kRingLagTailBytes + rf::kRingLagBarrierBytes : rf::kRingTailBytes + 32;
+    const int ncw = rf::kRingWarpsLag, nct = ncw * 32;
+    const size_t tail = rf::kRingLagTailBytes + rf::kRingLagBarrierBytes;
     for (int cs = 1; cs <= 8; cs *= 2) {
         const int slice = (g.row_vecs + cs - 1) / cs;
         if (cs > 1 && slice * (cs - 1) >= g.row_vecs) break;  // every rank must own >= 1 vector
         int nvt = 0;
-        if (g.kind == 1) {
-            nvt = (static_cast<int64_t>(27) * nct >= slice) ? 27 : 0;
-        } else if (g.kind == 2 && ncw != rf::kRingWarpsLag) {
-            const int q = ncw == 8 ? rf::kRingNvtLag8 : rf::kRingNvtLag16;
-            const bool bf = b->logits_dtype == RF_DTYPE_BF16 && o->dlogits_dtype == RF_DTYPE_BF16;
-            nvt = (bf && static_cast<int64_t>(q) * nct >= slice) ? q : 0;
-        } else {
-            const int* qs = g.kind == 2 ? rf::kRingNvtLag : rf::kRingNvtSmall;
-            const int nq = g.kind == 2 ? static_cast<int>(sizeof(rf::kRingNvtLag) / sizeof(int))
-                                       : static_cast<int>(sizeof(rf::kRingNvtSmall) / sizeof(int));
-            for (int i = 0; i < nq; ++i) {
-                if (static_cast<int64_t>(qs[i]) * nct >= slice) {
-                    nvt = qs[i];
-                    break;
-                }
+        for (int q : rf::kRingNvtLag)
+            if (static_cast<int64_t>(q) * nct >= slice) {
+                nvt = q;
+                break;
             }
-        }
         if (!nvt) continue;
-        const size_t cb = g.kind == 2 ? static_cast<size_t>(ncw) * 32 * rf::lag_vpc(nvt) * 16
-                                      : rf::ring_chunk_bytes(ncw, nvt);
+        const size_t cb = static_cast<size_t>(nct) * rf::lag_vpc(nvt) * 16;
         g.cs = cs;
         g.ncw = ncw;
         g.nvt = nvt;
         g.slice_vecs = slice;
         g.nchunks = static_cast<int>((slice + cb / 16 - 1) / (cb / 16));
         // [nslots x (chunk + full/empty barriers)] + row barriers + tail words
-        g.nslots = static_cast<int>((static_cast<size_t>(smem_cap) - tail) / (cb + 16));
+        g.nslots = static_cast<int>((static_cast<size_t>(max_optin_smem()) - tail) / (cb + 16));
         g.smem = static_cast<size_t>(g.nslots) * (cb + 16) + tail;
         g.ok = g.nslots >= 2;
         return g;
@@ -142,15 +106,12 @@ RingGeometry ring_geometry_kl(const rf_batch* b, const rf_outputs* o) {
     if (o->dlogits_row_stride < static_cast<int64_t>(g.row_vecs) * 8) return g;
     const int ncw = rf::kRingWarpsLag, nct = ncw * 32;
     const size_t tail = rf::kRingKLTailBytes + rf::kRingLagBarrierBytes;
-    // RF_KL_NVT caps the vectors per thread (A/B knob: 13 -> 4-CTA clusters at Qwen3)
-    int nvt_cap = rf::kRingNvtKL[2];
-    if (const char* e = std::getenv("RF_KL_NVT")) nvt_cap = std::atoi(e);
     for (int cs = 1; cs <= 8; ++cs) {  // any cluster size: the slice must fit the registers
         const int slice = (g.row_vecs + cs - 1) / cs;
         if (cs > 1 && slice * (cs - 1) >= g.row_vecs) break;
         int nvt = 0;
         for (int q : rf::kRingNvtKL)
-            if (q <= nvt_cap && static_cast<int64_t>(q) * nct >= slice) {
+            if (static_cast<int64_t>(q) * nct >= slice) {
                 nvt = q;
                 break;
             }
@@ -185,14 +146,13 @@ int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t s
             return k.val;
     int n = 0;
     const cudaError_t e = kind == 3 ? rf::ring_kl_max_clusters(ob, nvt, cs, smem, &n)
-                          : kind == 2 ? rf::ring_lag_max_clusters(ib, ob, ncw, nvt, cs, smem, &n)
-                                    : rf::ring_max_clusters(ib, ob, ncw, nvt, cs, smem, &n);
+                                    : rf::ring_lag_max_clusters(ib, ob, ncw, nvt, cs, smem, &n);
     if (e != cudaSuccess || n <= 0) {
         cudaGetLastError();
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        n = sms * (kind == 0 ? 2 : 1) / cs;
+        n = sms / cs;
     }
     cache.push_back({ib, ob, kind, ncw, nvt, cs, smem, n});
     return n;
@@ -246,16 +206,6 @@ WsLayout ws_layout(const rf_loss_config* c, const rf_batch* b, void* base) {
 }
 
 rf_status check_cuda(cudaError_t e) { return e == cudaSuccess ? RF_OK : RF_ERR_CUDA; }
-
-// sequence_product stats pass: the read-only online-softmax stream (K2st) by default;
-// RF_SP_STATS=ring selects the lag kernel in stats mode (A/B).
-static bool sp_stats_on_ring() {
-    static const bool ring = [] {
-        const char* e = std::getenv("RF_SP_STATS");
-        return e && std::string(e) == "ring";
-    }();
-    return ring;
-}
 
 // Per-phase cycle counters of the lag kernel (profiling aid): enabled by the
 // environment variable RF_DEBUG_COUNTERS=1, read with rf_debug_counters().
@@ -477,25 +427,16 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
         p.token_logp = o->token_logp ? o->token_logp : ws.lp;
         const int grid = generic_grid(b->num_tokens);
         p.mode = 1;
-        // Fast path: stats pass on the cluster ring kernel (lse per token, one read of
-        // the logits), sequence scalars, then the streaming dlogits pass — 6·V bytes
-        // per token.  Exact-KL and unaligned layouts take the generic kernel.
+        // Fast path (ring-compatible layout): K2st, the read-only online-softmax stats
+        // stream (lse per token, one read of the logits), the sequence scalars, then the
+        // K2w dlogits stream — 6·V bytes per token.  Exact KL and unaligned layouts take
+        // the generic kernel.
         RingGeometry g;
         if (kernel != RF_KERNEL_GENERIC && !needs_ref) g = ring_geometry(b, o);
         if (kernel == RF_KERNEL_RING && !g.ok) return RF_ERR_UNSUPPORTED_LAYOUT;
-        if (g.ok && g.kind == 2) {
-            p.slice_vecs = g.slice_vecs;
+        if (g.ok) {
             p.row_vecs = g.row_vecs;
-            p.nchunks = g.nchunks;
-            p.nslots = g.nslots;
-            if (sp_stats_on_ring()) {  // A/B arm: the lag kernel in stats mode
-                const int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
-                const int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-                if (rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s) != cudaSuccess)
-                    return RF_ERR_CUDA;
-            } else if (rf::launch_stream_stats(p, ib, s) != cudaSuccess) {
-                return RF_ERR_CUDA;
-            }
+            if (rf::launch_stream_stats(p, ib, s) != cudaSuccess) return RF_ERR_CUDA;
         } else {
             if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
         }
@@ -510,8 +451,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             KParams q = p;
             q.mode = 2;
             q.token_coef = ws.coef;
-            const cudaError_t e = (g.ok && g.kind == 2) ? rf::launch_stream_write(q, ib, ob, s)
-                                                         : rf::launch_generic(q, ib, ob, grid, s);
+            const cudaError_t e = g.ok ? rf::launch_stream_write(q, ib, ob, s) : rf::launch_generic(q, ib, ob, grid, s);
             if (e != cudaSuccess) return RF_ERR_CUDA;
             g_last_launches += 1;
         }
@@ -536,9 +476,8 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
                 p.xch_epoch = ++epoch;
             }
             int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
-            cudaError_t e = g.kind == 3   ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
-                            : g.kind == 2 ? rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s)
-                                          : rf::launch_ring(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
+            cudaError_t e = g.kind == 3 ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
+                                        : rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
             if (e == cudaErrorCooperativeLaunchTooLarge && p.vcs > 0) {
                 // the CTA groups need every CTA co-resident (e.g. SMs held by an MPS
                 // partition): the hardware-cluster version instead
@@ -549,7 +488,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
                 e = rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s);
             }
             if (e != cudaSuccess) return RF_ERR_CUDA;
-            nparts = g.kind >= 2 ? 2 * ncl : ncl;  // lag kernels: one partial row per scalar warp
+            nparts = 2 * ncl;  // lag kernels: one partial row per scalar warp
         } else {
             const int grid = generic_grid(b->num_tokens);
             if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;

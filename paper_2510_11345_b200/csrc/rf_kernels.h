@@ -6,30 +6,14 @@
 
 namespace rf {
 
-// Ring kernel (rf_ring.cu) configurations.  A CTA = NCW consumer warps + 1
-// producer warp; the CTA's row slice lives in registers (NVT 16-byte vectors
-// per consumer thread).
-//   small: 5 + 1 warps, two CTAs per SM (168 registers), NVT in {4, 16, 30}
-//   large: 11 + 1 warps, one CTA per SM (168 registers), NVT = 27
-constexpr int kRingWarpsSmall = 5;
-constexpr int kRingWarpsLarge = 11;
-constexpr int kRingNvtSmall[3] = {4, 16, 30};
-__host__ __device__ constexpr int ring_min_blocks(int ncw) { return ncw <= kRingWarpsSmall ? 2 : 1; }
-__host__ __device__ constexpr int ring_vpc(int nvt) { return nvt >= 9 ? 3 : 2; }  // vectors/thread/TMA chunk
-constexpr size_t ring_chunk_bytes(int ncw, int nvt) { return static_cast<size_t>(ncw) * 32 * ring_vpc(nvt) * 16; }
-constexpr size_t kRingTailBytes = 512;  // exchange / reduce / broadcast words
 // Lag configuration (rf_ring_lag.cu): NCW/4 consumer warpgroups + one support
 // warpgroup (TMA producer, two scalar warps, one idle) that hands its registers to
 // the consumers via setmaxnreg; one CTA per SM; the previous row's e parked in
 // TMEM.  Default NCW = 12 (3 consumer warps per SMSP, 152 registers each).
 constexpr int kRingWarpsLag = 12;
 constexpr int kRingNvtLag[4] = {4, 11, 12, 25};  // instances for NCW = 12 (11: V = 32,000 bf16, one CTA per row)
-constexpr int kRingNvtLag8 = 38;              // NCW = 8 (experiments, bf16 only)
-constexpr int kRingNvtLag16 = 19;             // NCW = 16 (experiments, bf16 only)
-#ifndef RF_LAG_REGS_SUPPORT
-#define RF_LAG_REGS_SUPPORT 56  // support warpgroup registers (A/B knob: 32 gives the consumers 160)
-#endif
-constexpr int kLagRegsSupport = RF_LAG_REGS_SUPPORT;
+// support warpgroup registers (32, giving the consumers 160, measured 10% slower)
+constexpr int kLagRegsSupport = 56;
 __host__ __device__ constexpr int lag_launch_regs(int ncw) {
     return ((65536 / ((ncw + 4) * 32)) / 8 * 8) > 248 ? 248 : ((65536 / ((ncw + 4) * 32)) / 8 * 8);
 }
@@ -39,17 +23,15 @@ __host__ __device__ constexpr int lag_regs_consumer(int ncw) {
                : ((lag_launch_regs(ncw) * (ncw + 4) * 32 - 128 * kLagRegsSupport) / (ncw * 32)) / 8 * 8;
 }
 __host__ __device__ constexpr unsigned lag_tmem_cols(int ncw) { return (512u / (ncw / 4)) / 8 * 8; }
-// vectors per thread per TMA chunk of the lag kernel (RF_LAG_VPC: A/B knob for NVT >= 9)
-#ifndef RF_LAG_VPC
-#define RF_LAG_VPC 5  // 30 KB chunks at 12 consumer warps: measured best of {2,3,4,5,7,9,13}
-#endif
-__host__ __device__ constexpr int lag_vpc(int nvt) { return (RF_LAG_VPC > 0 && nvt >= 9) ? RF_LAG_VPC : ring_vpc(nvt); }
-constexpr size_t kRingLagTailBytes = 1088;  // exchange / reduce / broadcast words + 4 exchange mbarriers
+// vectors per thread per TMA chunk of the lag kernels: 5 (30 KB chunks at 12
+// consumer warps, measured best of {2,3,4,5,7,9,13}) for the long rows, 2 for NVT = 4
+__host__ __device__ constexpr int lag_vpc(int nvt) { return nvt >= 9 ? 5 : 2; }
+constexpr size_t kRingLagTailBytes = 1088;  // exchange / reduce / broadcast words
 constexpr size_t kRingLagBarrierBytes = 48;
 
 // Exact-KL lag kernel (rf_ring_kl.cu): policy and reference rows co-resident,
 // 12 consumer warps, bf16 logits; NVT = 13 covers a quarter Qwen3 row (4-CTA cluster).
-constexpr int kRingNvtKL[3] = {4, 10, 13};  // 13: 4-CTA clusters at V=151,936 (5-CTA with RF_KL_NVT=10: -6%)
+constexpr int kRingNvtKL[3] = {4, 10, 13};  // 13: 4-CTA groups at V=151,936 (5-CTA groups at NVT 10 measured -6%)
 constexpr size_t kRingKLTailBytes = 2176;  // [4][8] 40-byte exchange slots + 5 x [2][NCW] partials + broadcast
 cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int nclusters, size_t smem,
                            cudaStream_t st);
@@ -66,9 +48,6 @@ cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt,
 constexpr int kGenericThreads = 256;
 constexpr int kGenericMaxGrid = 148 * 8;
 
-cudaError_t launch_ring(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
-                        size_t smem, cudaStream_t st);
-cudaError_t ring_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);
 cudaError_t launch_generic(const KParams& p, bool in_bf16, bool out_bf16, int grid, cudaStream_t st);
 // K2w (rf_stream.cu): dlogits from per-token coef + lse (needs p.row_vecs, ring-compatible layout)
 cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st);

@@ -1,7 +1,7 @@
 // rf_lag_common.cuh — pieces shared by the persistent TMEM-lag kernels
 // (rf_ring_lag.cu: loss + dlogits; rf_ring_kl.cu: the same with the exact-KL
-// reference row): A/B build knobs, barrier waits, the softmax-partial rescale
-// factor and the tcgen05 tensor-memory helpers.
+// reference row): barrier waits, the softmax-partial rescale factor and the
+// tcgen05 tensor-memory helpers.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -11,86 +11,19 @@ namespace rf {
 
 namespace {
 
-// Lanes of each scalar warp taking part in the per-row combine (32: shuffle
-// tree; 1: lane 0 alone).  Build-time knob for A/B runs (make variant).
-#ifndef RF_SCALAR_LANES
-#define RF_SCALAR_LANES 1
-#endif
-constexpr int kScalarLanes = RF_SCALAR_LANES;
-// Producer back-off while the ring is full (ns; 0 = spin) and the consumers' wait
-// flavour (1 = try_wait with a suspend-time hint, 0 = spin) — A/B knobs.
-#ifndef RF_PROD_SLEEP_NS
-#define RF_PROD_SLEEP_NS 256
-#endif
-#ifndef RF_CONS_SUSPEND
-#define RF_CONS_SUSPEND 1
-#endif
-__device__ __forceinline__ void cons_wait(uint32_t bar, uint32_t parity) {
-    if (RF_CONS_SUSPEND)
-        mbar_wait_sleep(bar, parity);
-    else
-        mbar_wait(bar, parity);
-}
-// Support-warp waits (producer empty slots, scalar partials): 1 = suspend-hint
-// try_wait, 0 = nanosleep polling (each poll costs issue slots on a consumer SMSP).
-#ifndef RF_SUPPORT_SUSPEND
-#define RF_SUPPORT_SUSPEND 1  // A/B on B200: +2% over 128 ns polling
-#endif
-__device__ __forceinline__ void support_wait(uint32_t bar, uint32_t parity, uint32_t ns) {
-    if (RF_SUPPORT_SUSPEND)
-        mbar_wait_sleep(bar, parity);
-    else
-        mbar_wait_backoff(bar, parity, ns);
-}
-// Parking e_t in TMEM: 0 = all columns then wait::st before streaming row t+1;
-// 1 = same stores, wait deferred to just before write_row(t); 2 = stores
-// interleaved with row t+1's copy-in (chunk by chunk), wait before write_row(t).
-#ifndef RF_PARK_MODE
-#define RF_PARK_MODE 2  // A/B on B200: +1.5% over 0, +1% over 1
-#endif
+// Waits.  Consumers and support warps block in mbarrier try_wait with a
+// suspend-time hint (measured +2% over nanosleep polling, which costs issue slots
+// on the consumers' SMSPs).
+__device__ __forceinline__ void cons_wait(uint32_t bar, uint32_t parity) { mbar_wait_sleep(bar, parity); }
+__device__ __forceinline__ void support_wait(uint32_t bar, uint32_t parity) { mbar_wait_sleep(bar, parity); }
 // Rescale factor 2^(m - mx) (m <= mx, log2 domain) of a partial softmax sum when
-// partials are combined.  RF_FAST_COMBINE (A/B knob): 1 = MUFU ex2 of the exact
-// (fp64) difference, relative error ~2^-22 — the class of every element's own
-// ex2.approx — instead of a ~200-cycle fp64 exp2 on the per-row critical path.
-#ifndef RF_FAST_COMBINE
-#define RF_FAST_COMBINE 1  // A/B on B200: +6.3% (the per-lane fp64 exp2 sat on every warp's row path)
-#endif
+// partials are combined: MUFU ex2 of the exact (fp64) difference, relative error
+// ~2^-22 — the class of every element's own ex2.approx.  (An fp64 exp2 here sat on
+// every warp's per-row critical path: measured 6.3% slower.)
 __device__ __forceinline__ double combine_factor(float m, float mx) {
     const double d = static_cast<double>(m) - static_cast<double>(mx);
-    if (RF_FAST_COMBINE) return static_cast<double>(ex2_approx(static_cast<float>(d)));
-    return exp2(d);
+    return static_cast<double>(ex2_approx(static_cast<float>(d)));
 }
-// Per-thread softmax sum: 0 = every vector's fp32 sum folded into fp64 (a 25-deep
-// F2F + DADD chain), 1 = four fp32 chains folded once (A/B knob).
-#ifndef RF_SUM_F32
-#define RF_SUM_F32 0
-#endif
-// Cluster exchange of the CTA partials: 1 = st.async + complete_tx on the peer's
-// mbarrier (no fence, no polling); 0 = sequence words with st.release / ld.acquire
-// polling (each poll invalidates L1, each release fences) — A/B knob.
-#ifndef RF_XCHG_MBAR
-#define RF_XCHG_MBAR 0
-#endif
-#ifndef RF_XCHG_TAG
-#define RF_XCHG_TAG 0  // 1: fence-free tagged 64-bit words (see rf_ring_lag.cu)
-#endif
-#ifndef RF_XCHG_SPIN
-#define RF_XCHG_SPIN 0  // exchange wait: 1 = try_wait polling with a 32 ns back-off
-#endif
-// Scalar lane fences its previous row's global output stores before waiting for the
-// next partials, so the exchange's release fence finds nothing outstanding (A/B knob).
-#ifndef RF_PREFENCE
-#define RF_PREFENCE 0
-#endif
-// Peer-partial poll: 1 = relaxed loads + one acquire fence after the last (an acquire
-// load invalidates L1 on every poll); 0 = ld.acquire per poll (A/B knob).
-#ifndef RF_XCHG_RELAXED_POLL
-#define RF_XCHG_RELAXED_POLL 0
-#endif
-// Write phase: straight-line stores for chunks with no padded / missing vectors.
-#ifndef RF_WRITE_FAST
-#define RF_WRITE_FAST 1  // A/B on B200: +6% (per-vector branches serialised the store math)
-#endif
 
 __device__ __forceinline__ void tmem_alloc(uint32_t smem_dst, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst), "r"(ncols)

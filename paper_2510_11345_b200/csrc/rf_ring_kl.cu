@@ -230,7 +230,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     const uint8_t* srf = reinterpret_cast<const uint8_t*>(p.ref_logits) +
                                          (row * p.ref_row_stride) * 2 + static_cast<size_t>(slice_begin) * 16;
                     for (int c = 0; c < nchunks; ++c) {
-                        if (uses >= static_cast<uint32_t>(nslots)) support_wait(bar_empty + 8 * s, phase, 256);
+                        if (uses >= static_cast<uint32_t>(nslots)) support_wait(bar_empty + 8 * s, phase);
                         const int nv = min(CHUNK_VECS, slice_len - c * CHUNK_VECS);
                         const uint32_t bytes = static_cast<uint32_t>(nv) * 16;
                         mbar_arrive_expect_tx(bar_full + 8 * s, 2 * bytes);
@@ -263,8 +263,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 const TokenPre pre = token_pre(p, t, seq);
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
-                if (RF_PREFENCE) fence_acq_rel_cluster();  // drain this lane's output stores while idle
-                support_wait(bar_red + 8 * par, ph, 128);
+                support_wait(bar_red + 8 * par, ph);
                 // CTA partials, warp order
                 float Mw = -CUDART_INF_F, Myw = -CUDART_INF_F;
                 for (int w = 0; w < NCW; ++w) {

@@ -1,10 +1,10 @@
-// rf_ring_lag.cu — K2 "lag" variant: the fused off-policy loss + dlogits kernel
-// with the per-row softmax/coefficient round trip taken off the critical path.
+// rf_ring_lag.cu — K2: the fused off-policy loss + dlogits kernel, with the per-row
+// softmax/coefficient round trip taken off the consumers' critical path.
 //
-// Same data path as rf_ring.cu (one HBM read of every logits row, one HBM write of
-// its dlogits row; TMA bulk loads into a shared-memory ring; the row slice held
-// in the register file during the exp sweep), but the consumer warps never wait
-// for the row coefficient of the row they just reduced:
+// One HBM read of every logits row, one HBM write of its dlogits row: TMA bulk
+// loads stream each CTA's slice of the row into a shared-memory ring, the slice is
+// held in the register file for the max and exp sweeps, and the consumer warps
+// never wait for the coefficient of the row they just reduced:
 //
 //   row i   : copy-in + max + exp sweep in registers -> warp partials (M,S) -> scalar warp
 //   row i+1 : copy-in (parking e_i in TENSOR MEMORY chunk by chunk, tcgen05.st,
@@ -17,8 +17,8 @@
 // surrogate math, losses.cpp:264-320) have a whole row of streaming to finish.
 // One CTA per SM: 12 consumer warps (152 registers via setmaxnreg) + one support
 // warpgroup (TMA producer, two scalar warps for even/odd rows, one idle warp);
-// 2-CTA clusters for the Qwen3 vocabulary.  Build-time A/B knobs and their measured
-// outcomes: rf_lag_common.cuh, profiles/r01_ab/ab_log.txt.
+// 2-CTA clusters for the Qwen3 vocabulary.  The alternatives measured against
+// each design choice are logged in profiles/r01_ab/ab_log.txt.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -66,7 +66,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         uint32_t seq;
     };
     XSlot* xslot = reinterpret_cast<XSlot*>(tail);                  // [4][8]
-    const uint32_t xbar = smem_u32(tail + 1024);                     // [4] exchange mbarriers (RF_XCHG_MBAR)
     double* redS = reinterpret_cast<double*>(tail + 512);           // [2][NCW]
     float* redM = reinterpret_cast<float*>(tail + 512 + 16 * NCW);  // [2][NCW]
     struct Bcast {
@@ -99,7 +98,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             xslot[q].S = 0.0;  // tag 0 in both words: never a live use
             xslot[q].seq = 0u;
         }
-        for (int q = 0; q < 4; ++q) mbar_init(xbar + 8 * q, 1);  // the local scalar's arrive.expect_tx
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -138,10 +136,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 for (int c = 0; c < nchunks; ++c) {
                     if (uses >= static_cast<uint32_t>(nslots)) {
                         if (kPhaseCounters && p.dbg) pc.start();
-                        if (RF_PROD_SLEEP_NS > 0)
-                            support_wait(bar_empty + 8 * s, phase, RF_PROD_SLEEP_NS);
-                        else
-                            mbar_wait(bar_empty + 8 * s, phase);
+                        support_wait(bar_empty + 8 * s, phase);
                         if (kPhaseCounters && p.dbg) pc.lap(dw);
                     }
                     const int nv = min(CHUNK_VECS, slice_len - c * CHUNK_VECS);
@@ -167,8 +162,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         // --------------------------------- scalar ---------------------------------
         // Two scalar warps: warp NCW+1 owns the even rows of this cluster, NCW+2 the
         // odd ones (row parity == buffer parity), so each has two rows of
-        // streaming to finish its exchange + fp64 math.
-        {
+        // streaming to finish its exchange + fp64 math.  Lane 0 does the work (a
+        // 32-lane shuffle-tree combine measured no faster).
+        if (lane == 0) {
             const uint32_t which = static_cast<uint32_t>(warp - NCW - 1);
             Partials part;
             part.zero();
@@ -178,118 +174,46 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             pc.start();
             const long long t_begin = pc.t;
             for (int64_t t = cid + static_cast<int64_t>(which) * ncl; t < p.T; t += 2 * ncl, row_iter += 2) {
-                if (kScalarLanes == 1 && lane != 0) break;
-                int32_t tok = -1;
-                bool tok_ok = false;
-                float x_tok = 0.0f;
-                TokenPre pre{};
-                if (lane == 0) {  // issue the per-token loads before waiting
-                    const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
-                    tok = p.token_ids[t];
-                    tok_ok = tok >= 0 && tok < p.V;
-                    x_tok = tok_ok ? load_logit(p.logits, row * p.row_stride + tok, IN_BF16) : 0.0f;
-                    pre = token_pre(p, t, p.seq_of_token[t]);
-                }
+                // issue the per-token loads before waiting
+                const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
+                const int32_t tok = p.token_ids[t];
+                const bool tok_ok = tok >= 0 && tok < p.V;
+                const float x_tok = tok_ok ? load_logit(p.logits, row * p.row_stride + tok, IN_BF16) : 0.0f;
+                const TokenPre pre = token_pre(p, t, p.seq_of_token[t]);
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                if (RF_PREFENCE) fence_acq_rel_cluster();  // drain this lane's output stores while idle
-                support_wait(bar_red + 8 * par, ph, 128);
+                support_wait(bar_red + 8 * par, ph);
                 if (kPhaseCounters && p.dbg) pc.lap(d_red);
-                float Mw;
-                double Sw;
-                if constexpr (kScalarLanes > 1) {
-                    // combine the consumer warps' partials across the scalar warp's lanes
-                    // (fixed shuffle tree: deterministic)
-                    const float Mq = lane < NCW ? redM[par * NCW + lane] : -CUDART_INF_F;
-                    const double Sq = lane < NCW ? redS[par * NCW + lane] : 0.0;
-                    Mw = Mq;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
-                    Sw = (Sq != 0.0) ? Sq * combine_factor(Mq, Mw) : 0.0;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) Sw += __shfl_xor_sync(0xffffffffu, Sw, o);
-                    if (lane != 0) {  // park at the row's closing __syncwarp (no polling)
-                        __syncwarp();
-                        continue;
-                    }
-                } else {  // lane 0 alone, sequential in warp order
-                    Mw = -CUDART_INF_F;
-                    for (int w = 0; w < NCW; ++w) Mw = fmaxf(Mw, redM[par * NCW + w]);
-                    Sw = 0.0;
-                    for (int w = 0; w < NCW; ++w) {
-                        const double sw = redS[par * NCW + w];
-                        if (sw != 0.0)
-                            Sw += sw * combine_factor(redM[par * NCW + w], Mw);
-                    }
+                // combine the consumer warps' partials, sequential in warp order
+                float Mw = -CUDART_INF_F;
+                for (int w = 0; w < NCW; ++w) Mw = fmaxf(Mw, redM[par * NCW + w]);
+                double Sw = 0.0;
+                for (int w = 0; w < NCW; ++w) {
+                    const double sw = redS[par * NCW + w];
+                    if (sw != 0.0) Sw += sw * combine_factor(redM[par * NCW + w], Mw);
                 }
                 double Mc = static_cast<double>(Mw), Sc = Sw;
                 if (csize > 1) {
-                    if (RF_XCHG_MBAR) {
-                        // st.async the (S, M) partial into every peer's slot, completing bytes
-                        // on the peer's exchange mbarrier of this row slot; then arm the local
-                        // one and wait for every peer's partial of this row
-                        const uint32_t xs = row_iter & 3;
-                        const XSlot* mine = &xslot[xs * 8 + rank];
-                        for (uint32_t q = 0; q < csize; ++q) {
-                            if (q == rank) continue;
-                            const uint32_t rb = mapa(xbar + 8 * xs, q);
-                            st_async_f64(mapa(smem_u32(&mine->S), q), Sw, rb);
-                            st_async_f32(mapa(smem_u32(&mine->M), q), Mw, rb);
-                        }
-                        mbar_arrive_expect_tx(xbar + 8 * xs, 12u * (csize - 1));
-                        if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                        if (RF_XCHG_SPIN)
-                            mbar_wait_backoff(xbar + 8 * xs, (row_iter >> 2) & 1, 32);
-                        else
-                            support_wait(xbar + 8 * xs, (row_iter >> 2) & 1, 32);
-                        if (kPhaseCounters && p.dbg) pc.lap(d_x);
-                    } else if (RF_XCHG_TAG) {
-                        // fence-free: two single-copy-atomic 64-bit words per peer, each
-                        // carrying the slot's use tag — (S with the tag in its 8 low mantissa
-                        // bits, 2^-44 relative) and (M, tag) — polled until both match
-                        const uint32_t xs = row_iter & 3;
-                        const uint32_t tag = (row_iter >> 2) + 1;
-                        const uint64_t w0 =
-                            (static_cast<uint64_t>(__double_as_longlong(Sw)) & ~0xffull) | (tag & 0xffu);
-                        const uint64_t w1 = static_cast<uint64_t>(__float_as_uint(Mw)) | (static_cast<uint64_t>(tag) << 32);
-                        XSlot* mine = &xslot[xs * 8 + rank];
-                        for (uint32_t q = 0; q < csize; ++q) {
-                            if (q == rank) continue;
-                            st_relaxed_cluster_u64(mapa(smem_u32(&mine->S), q), w0);
-                            st_relaxed_cluster_u64(mapa(smem_u32(&mine->M), q), w1);
-                        }
-                        if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                        for (uint32_t q = 0; q < csize; ++q) {
-                            if (q == rank) continue;
-                            const uint32_t a0 = smem_u32(&xslot[xs * 8 + q].S), a1 = smem_u32(&xslot[xs * 8 + q].M);
-                            while ((ld_relaxed_cluster_u64(a1) >> 32) != tag ||
-                                   (ld_relaxed_cluster_u64(a0) & 0xffu) != (tag & 0xffu))
-                                __nanosleep(32);
-                        }
-                        if (kPhaseCounters && p.dbg) pc.lap(d_x);
-                    } else {
-                        const uint32_t slot = (row_iter & 3) * 8 + rank;
-                        XSlot* mine = &xslot[slot];
-                        for (uint32_t q = 0; q < csize; ++q) {  // push (S, M) to every peer, then publish
-                            if (q == rank) continue;
-                            st_cluster_f64(mapa(smem_u32(&mine->S), q), Sw);
-                            st_cluster_f32(mapa(smem_u32(&mine->M), q), Mw);
-                            st_release_cluster_u32(mapa(smem_u32(&mine->seq), q), row_iter + 1);
-                        }
-                        if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                        for (uint32_t q = 0; q < csize; ++q) {  // wait for every peer's partial of this row
-                            if (q == rank) continue;
-                            const uint32_t a = smem_u32(&xslot[(row_iter & 3) * 8 + q].seq);
-                            if (RF_XCHG_RELAXED_POLL) {
-                                while (ld_relaxed_cluster_u32(a) != row_iter + 1) __nanosleep(32);
-                            } else {
-                                while (ld_acquire_cluster_u32(a) != row_iter + 1) __nanosleep(32);
-                            }
-                        }
-                        if (RF_XCHG_RELAXED_POLL) fence_acq_rel_cluster();  // one acquire for all polls
-                        if (kPhaseCounters && p.dbg) pc.lap(d_x);
+                    // push (S, M) to every peer's slot [row % 4][my rank], publish it with a
+                    // release store of the sequence word row + 1, then poll the peers' words
+                    // with acquire loads (an st.async + remote-mbarrier variant measured 4%
+                    // slower: longer wake-up on the coefficient's critical path)
+                    const uint32_t slot = (row_iter & 3) * 8 + rank;
+                    XSlot* mine = &xslot[slot];
+                    for (uint32_t q = 0; q < csize; ++q) {
+                        if (q == rank) continue;
+                        st_cluster_f64(mapa(smem_u32(&mine->S), q), Sw);
+                        st_cluster_f32(mapa(smem_u32(&mine->M), q), Mw);
+                        st_release_cluster_u32(mapa(smem_u32(&mine->seq), q), row_iter + 1);
                     }
+                    if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                    for (uint32_t q = 0; q < csize; ++q) {
+                        if (q == rank) continue;
+                        const uint32_t a = smem_u32(&xslot[(row_iter & 3) * 8 + q].seq);
+                        while (ld_acquire_cluster_u32(a) != row_iter + 1) __nanosleep(32);
+                    }
+                    if (kPhaseCounters && p.dbg) pc.lap(d_x);
                     float Mx = -CUDART_INF_F;
                     for (uint32_t q = 0; q < csize; ++q)
                         Mx = fmaxf(Mx, (q == rank) ? Mw : xslot[(row_iter & 3) * 8 + q].M);
@@ -302,15 +226,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     Mc = static_cast<double>(Mx);
                 }
                 const double lse = 0.69314718055994530942 * (Mc + log2(Sc));  // natural-log lse
-                if (p.mode == 1) {  // stats pass (sequence_product): lse and lp per token only
-                    if (rank == 0) {
-                        p.tok_lse[t] = lse;
-                        p.token_logp[t] = tok_ok ? static_cast<double>(x_tok) - lse : CUDART_NAN;
-                        if (!tok_ok) atomicOr(p.status, RF_DEVSTAT_TOKEN_OUT_OF_RANGE);
-                    }
-                    mbar_arrive(bar_bc + 8 * par);  // keeps the consumers' row pacing
-                    continue;
-                }
                 TokenResult tr;
                 double lp = CUDART_NAN;
                 if (!tok_ok) {
@@ -341,11 +256,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     part.add_token(tr, 0.0);
                 }
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
-                if constexpr (kScalarLanes > 1) __syncwarp();
             }
-            if (lane == 0 && rank == 0)
-                part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
-            if (kPhaseCounters && p.dbg && lane == 0) {
+            if (rank == 0) part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
+            if (kPhaseCounters && p.dbg) {
                 atomicAdd(p.dbg + 6, d_red);
                 atomicAdd(p.dbg + 7, d_x);
                 atomicAdd(p.dbg + 8, d_math);
@@ -393,7 +306,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         auto stream_row = [&](uint32_t row_iter, bool park_prev) -> float {
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                if (RF_PARK_MODE == 2 && park_prev && p.mode != 1) {  // park the previous row's e, chunk by chunk
+                if (park_prev) {  // park the previous row's e in TMEM, chunk by chunk
 #pragma unroll
                     for (int jj = 0; jj < VPC; ++jj)
                         if (c * VPC + jj < NVT) tmem_st4(tm + 4 * (c * VPC + jj), r[c * VPC + jj]);
@@ -448,25 +361,12 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             const float Mt = (M == -CUDART_INF_F) ? 0.0f : M;
             const float C = Mt * 1.4426950408889634f;
             const uint64_t negC2 = pk2(-C, -C);
+            // every vector's packed fp32 pair sum folded into fp64
             double S = 0.0;
-            if (RF_SUM_F32) {  // four fp32 chains (two packed pairs), folded into fp64 once
-                uint64_t A0 = pk2(0.0f, 0.0f), A1 = pk2(0.0f, 0.0f);
 #pragma unroll
-                for (int j = 0; j < NVT; ++j) {
-                    const uint64_t acc = vec_exp<IN_BF16>(r[j], L2, negC2);
-                    if (j & 1)
-                        A1 = fadd2(A1, acc);
-                    else
-                        A0 = fadd2(A0, acc);
-                }
-                S = (static_cast<double>(lo2(A0)) + static_cast<double>(hi2(A0))) +
-                    (static_cast<double>(lo2(A1)) + static_cast<double>(hi2(A1)));
-            } else {
-#pragma unroll
-                for (int j = 0; j < NVT; ++j) {
-                    const uint64_t acc = vec_exp<IN_BF16>(r[j], L2, negC2);
-                    S += static_cast<double>(lo2(acc) + hi2(acc));
-                }
+            for (int j = 0; j < NVT; ++j) {
+                const uint64_t acc = vec_exp<IN_BF16>(r[j], L2, negC2);
+                S += static_cast<double>(lo2(acc) + hi2(acc));
             }
             const float Mr = (S == 0.0) ? -CUDART_INF_F : C;
             // warp reduction of (C, S) pairs in the log2 domain; each warp hands its
@@ -493,7 +393,6 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             if (dbg) pcc.lap(dph[4]);
             cons_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
             if (dbg) pcc.lap(dph[3]);
-            if (p.mode == 1) return;  // stats pass: no dlogits
             const Bcast* bc = bcs + par;
             const float lseL = bc->lseL;
             const float negk = bc->negk;
@@ -517,7 +416,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                         if (c * VPC + h < NVT) tmem_ld4(tm + 4 * (c * VPC + h), e[h]);
                 }
                 uint8_t* dc = dthr + static_cast<size_t>(c) * CHUNK_VECS * EPV * OES;
-                if (RF_WRITE_FAST && c * VPC + VPC <= jfull) {
+                if (c * VPC + VPC <= jfull) {  // straight-line stores (+6% over per-vector branches)
 #pragma unroll
                     for (int h = 0; h < VPC; ++h)
                         store_vec<OUT_BF16, EPV>(dc + static_cast<size_t>(h) * NCT * EPV * OES, e[h], f2, IN_BF16);
@@ -554,16 +453,14 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         while (t < p.T) {
             // park e_t in TMEM, stream row t + ncl (if any), then write row t from TMEM
             const int64_t tn = t + ncl;
-            if (RF_PARK_MODE != 2 || tn >= p.T) {
+            if (tn >= p.T) {  // last row: nothing to stream, park it all now
 #pragma unroll
-                for (int j = 0; j < NVT; ++j)
-                    if (p.mode != 1) tmem_st4(tm + 4 * j, r[j]);
-                if (RF_PARK_MODE == 0) tmem_wait_st();
+                for (int j = 0; j < NVT; ++j) tmem_st4(tm + 4 * j, r[j]);
             }
             if (dbg) pcc.lap(dph[2]);
             float Cn = 0.f;
             if (tn < p.T) Cn = stream_row(it + 1, true);
-            if (RF_PARK_MODE != 0) tmem_wait_st();  // e_t must be in TMEM before write_row reads it back
+            tmem_wait_st();  // e_t must be in TMEM before write_row reads it back
             write_row(t, it, C);
             C = Cn;
             t = tn;
@@ -615,9 +512,6 @@ cudaError_t lag_cfg(const KParams& p, int ncw, int nvt, int cs, int ncl, size_t 
             case kRingNvtLag[3]: return launch_lag_t<IB, OB, kRingWarpsLag, kRingNvtLag[3]>(p, cs, ncl, smem, st, maxc);
         }
     }
-    if (IB && OB && ncw == 8 && nvt == kRingNvtLag8) return launch_lag_t<IB, OB, 8, kRingNvtLag8>(p, cs, ncl, smem, st, maxc);
-    if (IB && OB && ncw == 16 && nvt == kRingNvtLag16)
-        return launch_lag_t<IB, OB, 16, kRingNvtLag16>(p, cs, ncl, smem, st, maxc);
     return cudaErrorInvalidValue;
 }
 

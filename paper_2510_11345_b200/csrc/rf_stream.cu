@@ -7,11 +7,11 @@
 //
 // A pure streaming kernel: one CTA per row at a time (persistent), 128-bit
 // non-allocating loads, several loads in flight per thread, packed FFMA2 + one
-// MUFU ex2 per element, 128-bit streaming stores.  2·V bytes read + 2·V written.
+// MUFU ex2 per element + packed FMUL2 by −k, 128-bit streaming stores.  2·V bytes
+// read + 2·V written.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <math_constants.h>
 
 #include "rf_device.cuh"
@@ -34,64 +34,6 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 
 constexpr int kStreamThreads = 256;
 
-// 2^a for a packed pair on the FMA pipe (offloads the MUFU, which bounds the
-// read-only stats stream: 8 ex2 per 16-byte vector).  Round-to-nearest split
-// a = n + f (magic-number add), degree-5 near-minimax polynomial for 2^f on
-// [-1/2, 1/2] (max relative error 2.3e-7, the ex2.approx class), exponent added
-// as integer bits.  Arguments are clamped at -125 (2^-125 stands in for 0).
-__device__ __forceinline__ uint64_t ex2_poly2(uint64_t a) {
-    const float a0 = fmaxf(lo2(a), -125.0f), a1 = fmaxf(hi2(a), -125.0f);
-    const uint64_t x = pk2(a0, a1);
-    const uint64_t j = fadd2(x, pk2(12582912.0f, 12582912.0f));  // 1.5·2^23 + n
-    const uint64_t r = fadd2(j, pk2(-12582912.0f, -12582912.0f)); // n as float
-    const uint64_t fr = ffma2(r, pk2(-1.0f, -1.0f), x);            // f = a - n
-    uint64_t q = ffma2(pk2(0.001327647129073739f, 0.001327647129073739f), fr,
-                       pk2(0.009675540961325169f, 0.009675540961325169f));
-    q = ffma2(q, fr, pk2(0.05550713092088699f, 0.05550713092088699f));
-    q = ffma2(q, fr, pk2(0.24022120237350464f, 0.24022120237350464f));
-    q = ffma2(q, fr, pk2(0.6931469440460205f, 0.6931469440460205f));
-    q = ffma2(q, fr, pk2(1.0000001192092896f, 1.0000001192092896f));
-    // bits(j) << 23 == n << 23 (the magic's own bits vanish mod 2^32)
-    const uint32_t lo = static_cast<uint32_t>(q) + (static_cast<uint32_t>(j) << 23);
-    const uint32_t hi = static_cast<uint32_t>(q >> 32) + (static_cast<uint32_t>(j >> 32) << 23);
-    return static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
-}
-
-// vectors in flight per thread: RF_STREAM_UNROLL=4|8 (A/B knob, default 4)
-int stream_unroll() {
-    static const int u = [] {
-        const char* e = std::getenv("RF_STREAM_UNROLL");
-        return (e && std::atoi(e) == 8) ? 8 : 4;
-    }();
-    return u;
-}
-
-// min resident CTAs per SM the register allocation is bounded for: the read-only
-// stats stream wants every slot filled (8 CTAs, 32 registers: 6.1 vs 5.2 TB/s), the
-// write stream its unspilled 68 registers (4 CTAs: 6.1 vs 5.5 TB/s at 8).
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
-int stats_minb() {
-    static const int m = env_int("RF_STATS_MINB", 8);
-    return m;
-}
-// RF_STATS_POLY=1: one element pair per vector through ex2_poly2 (A/B knob)
-int stats_poly() {
-    static const int m = env_int("RF_STATS_POLY", 0);
-    return m;
-}
-// RF_WRITE_POLY=1: the same split in the write stream (A/B knob)
-int write_poly() {
-    static const int m = env_int("RF_WRITE_POLY", 0);
-    return m;
-}
-int stream_minb() {
-    static const int m = env_int("RF_STREAM_MINB", 1);
-    return m;
-}
-
 // persistent grid: every CTA resident (grid = SMs x occupancy)
 template <typename K>
 int resident_grid(K kernel, int64_t T) {
@@ -104,8 +46,16 @@ int resident_grid(K kernel, int64_t T) {
 
 }  // namespace
 
-template <bool IN_BF16, bool OUT_BF16, int kStreamUnroll, int MINB, bool POLY = false>
-__global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(const __grid_constant__ KParams p) {
+// Vectors in flight per thread (4 measured best of {4, 8}); resident CTAs per SM
+// the register allocation is bounded for: the read-only stats stream wants every
+// slot filled (8 CTAs, 32 registers: 6.1 vs 5.2 TB/s at 4), the write stream its
+// unspilled registers (6.1 vs 5.5 TB/s when bounded for 8).
+constexpr int kStreamUnroll = 4;
+constexpr int kStatsMinBlocks = 8;
+constexpr int kWriteMinBlocks = 1;
+
+template <bool IN_BF16, bool OUT_BF16>
+__global__ void __launch_bounds__(kStreamThreads, kWriteMinBlocks) stream_write_kernel(const __grid_constant__ KParams p) {
     constexpr int EPV = IN_BF16 ? 8 : 4;
     constexpr size_t IES = IN_BF16 ? 2 : 4;
     constexpr size_t OES = OUT_BF16 ? 2 : 4;
@@ -123,10 +73,10 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(cons
         const double lse = p.tok_lse[t];
         const int32_t tok = p.token_ids[t];
         const float lseL = static_cast<float>(lse * 1.4426950408889634);
-        const float negk = static_cast<float>(-k);
         const bool zero = (k == 0.0);
+        const float f = zero ? 0.0f : static_cast<float>(-k);
         const uint64_t negC2 = pk2(-lseL, -lseL);
-        const uint64_t f2 = pk2(zero ? 0.0f : negk, zero ? 0.0f : negk);
+        const uint64_t f2 = pk2(f, f);
         for (int v0 = tid; v0 < row_vecs; v0 += kStreamThreads * kStreamUnroll) {
             uint4 x[kStreamUnroll];
 #pragma unroll
@@ -138,34 +88,51 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(cons
             for (int u = 0; u < kStreamUnroll; ++u) {
                 const int v = v0 + u * kStreamThreads;
                 if (v >= row_vecs) break;
-                // e = 2^(x·L - lse·L) = p, then out = -k·p via the shared packed store path
-                uint4 e = x[u];
-                uint32_t w[4] = {e.x, e.y, e.z, e.w};
+                // p = 2^(x·log2e − lse·log2e) kept in f32 and scaled by −k before the one
+                // rounding to the output dtype (p itself is ~1/V: as f16 it would be
+                // subnormal, ~3% relative error per entry)
+                uint8_t* d = dst + static_cast<size_t>(v) * EPV * OES;
+                const bool full = (v != tail_vec || tail_valid == EPV);
                 if (IN_BF16) {
+                    const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+                    uint64_t o[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t a = ffma2(bf16x2_to_f32x2(w[q]), L2, negC2);
-                        if (POLY && q == 3) {
-                            const uint64_t e = ex2_poly2(a);
-                            w[q] = pack_f16x2(lo2(e), hi2(e));
+                        o[q] = fmul2(pk2(ex2_approx(lo2(a)), ex2_approx(hi2(a))), f2);
+                    }
+                    if (full) {
+                        if (OUT_BF16) {
+                            stg128_cs(d, make_uint4(pack_bf16x2(lo2(o[0]), hi2(o[0])), pack_bf16x2(lo2(o[1]), hi2(o[1])),
+                                                    pack_bf16x2(lo2(o[2]), hi2(o[2])), pack_bf16x2(lo2(o[3]), hi2(o[3]))));
                         } else {
-                            w[q] = pack_f16x2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
+                            stg128_cs(d, make_uint4(static_cast<uint32_t>(o[0]), static_cast<uint32_t>(o[0] >> 32),
+                                                    static_cast<uint32_t>(o[1]), static_cast<uint32_t>(o[1] >> 32)));
+                            stg128_cs(d + 16, make_uint4(static_cast<uint32_t>(o[2]), static_cast<uint32_t>(o[2] >> 32),
+                                                         static_cast<uint32_t>(o[3]), static_cast<uint32_t>(o[3] >> 32)));
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            if (q < tail_valid) {
+                                const float val = (q & 1) ? hi2(o[q >> 1]) : lo2(o[q >> 1]);
+                                if (OUT_BF16)
+                                    reinterpret_cast<__nv_bfloat16*>(d)[q] = __float2bfloat16_rn(val);
+                                else
+                                    reinterpret_cast<float*>(d)[q] = val;
+                            }
                         }
                     }
                 } else {
-                    const uint64_t a01 = ffma2(pk2(__uint_as_float(w[0]), __uint_as_float(w[1])), L2, negC2);
-                    const uint64_t a23 = ffma2(pk2(__uint_as_float(w[2]), __uint_as_float(w[3])), L2, negC2);
-                    w[0] = __float_as_uint(ex2_approx(lo2(a01)));
-                    w[1] = __float_as_uint(ex2_approx(hi2(a01)));
-                    w[2] = __float_as_uint(ex2_approx(lo2(a23)));
-                    w[3] = __float_as_uint(ex2_approx(hi2(a23)));
+                    const uint64_t a01 = ffma2(pk2(__uint_as_float(x[u].x), __uint_as_float(x[u].y)), L2, negC2);
+                    const uint64_t a23 = ffma2(pk2(__uint_as_float(x[u].z), __uint_as_float(x[u].w)), L2, negC2);
+                    const uint4 e = make_uint4(__float_as_uint(ex2_approx(lo2(a01))), __float_as_uint(ex2_approx(hi2(a01))),
+                                               __float_as_uint(ex2_approx(lo2(a23))), __float_as_uint(ex2_approx(hi2(a23))));
+                    if (full)
+                        store_vec<OUT_BF16, 4>(d, e, f2, false);
+                    else
+                        store_vec_partial<OUT_BF16, 4>(d, e, f, false, tail_valid);
                 }
-                e = make_uint4(w[0], w[1], w[2], w[3]);
-                uint8_t* d = dst + static_cast<size_t>(v) * EPV * OES;
-                if (v != tail_vec || tail_valid == EPV)
-                    store_vec<OUT_BF16, EPV>(d, e, f2, IN_BF16);
-                else
-                    store_vec_partial<OUT_BF16, EPV>(d, e, zero ? 0.0f : negk, IN_BF16, tail_valid);
                 if (v == tok / EPV && tok >= 0 && tok < p.V) {  // sampled token, same thread: k(1 - p_tok)
                     const double lp = static_cast<double>(load_logit(p.logits, row * p.row_stride + tok, IN_BF16)) - lse;
                     const float tv = zero ? 0.0f : static_cast<float>(k - k * exp(lp));
@@ -185,8 +152,8 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_write_kernel(cons
 // its running max, S = Σ 2^(x·log2e − C) in fp64 (fp32 per batch of kStreamUnroll
 // vectors, rescaled by ex2 of the exact float offset difference when the max moves).
 // 2·V bytes read per token.
-template <bool IN_BF16, int kStreamUnroll, int MINB, bool POLY = false>
-__global__ void __launch_bounds__(kStreamThreads, MINB) stream_stats_kernel(const __grid_constant__ KParams p) {
+template <bool IN_BF16>
+__global__ void __launch_bounds__(kStreamThreads, kStatsMinBlocks) stream_stats_kernel(const __grid_constant__ KParams p) {
     constexpr int EPV = IN_BF16 ? 8 : 4;
     constexpr size_t IES = IN_BF16 ? 2 : 4;
     constexpr float kL2e = 1.4426950408889634f;
@@ -240,8 +207,7 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_stats_kernel(cons
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t a = ffma2(bf16x2_to_f32x2(w[q]), L2, negC2);
-                        const uint64_t e = (POLY && q == 3) ? ex2_poly2(a)
-                                                             : pk2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
+                        const uint64_t e = pk2(ex2_approx(lo2(a)), ex2_approx(hi2(a)));
                         acc = (u == 0 && q == 0) ? e : fadd2(acc, e);
                     }
                 } else {
@@ -284,63 +250,33 @@ __global__ void __launch_bounds__(kStreamThreads, MINB) stream_stats_kernel(cons
     }
 }
 
-template <int U, int MINB>
-cudaError_t launch_stats_u(const KParams& p, bool in_bf16, cudaStream_t st) {
+cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st) {
     if (in_bf16) {
-        auto k = stream_stats_kernel<true, U, MINB>;
+        auto k = stream_stats_kernel<true>;
         k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
     } else {
-        auto k = stream_stats_kernel<false, U, MINB>;
+        auto k = stream_stats_kernel<false>;
         k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
     }
     return cudaGetLastError();
 }
 
-template <bool IB, bool OB, int U, int MINB>
+template <bool IB, bool OB>
 void launch_write_t(const KParams& p, cudaStream_t st) {
-    auto k = stream_write_kernel<IB, OB, U, MINB>;
+    auto k = stream_write_kernel<IB, OB>;
     k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
 }
 
-template <int U, int MINB>
-cudaError_t launch_write_u(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st) {
-    if (in_bf16 && out_bf16)
-        launch_write_t<true, true, U, MINB>(p, st);
-    else if (in_bf16)
-        launch_write_t<true, false, U, MINB>(p, st);
-    else if (out_bf16)
-        launch_write_t<false, true, U, MINB>(p, st);
-    else
-        launch_write_t<false, false, U, MINB>(p, st);
-    return cudaGetLastError();
-}
-
-// A/B knobs: RF_STREAM_UNROLL (vectors in flight per thread), RF_STATS_MINB and
-// RF_STREAM_MINB (min resident CTAs per SM of the stats / write kernels).
-cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st) {
-    const int mb = stats_minb();
-    if (in_bf16 && stats_poly()) {
-        auto k = stream_stats_kernel<true, 4, 8, true>;
-        k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
-        return cudaGetLastError();
-    }
-    if (stream_unroll() == 8) return launch_stats_u<8, 1>(p, in_bf16, st);
-    if (mb == 8) return launch_stats_u<4, 8>(p, in_bf16, st);
-    if (mb == 6) return launch_stats_u<4, 6>(p, in_bf16, st);
-    return launch_stats_u<4, 1>(p, in_bf16, st);
-}
-
 cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, cudaStream_t st) {
-    const int mb = stream_minb();
-    if (in_bf16 && out_bf16 && write_poly()) {
-        auto k = stream_write_kernel<true, true, 4, 1, true>;
-        k<<<resident_grid(k, p.T), kStreamThreads, 0, st>>>(p);
-        return cudaGetLastError();
-    }
-    if (stream_unroll() == 8) return launch_write_u<8, 1>(p, in_bf16, out_bf16, st);
-    if (mb == 8) return launch_write_u<4, 8>(p, in_bf16, out_bf16, st);
-    if (mb == 6) return launch_write_u<4, 6>(p, in_bf16, out_bf16, st);
-    return launch_write_u<4, 1>(p, in_bf16, out_bf16, st);
+    if (in_bf16 && out_bf16)
+        launch_write_t<true, true>(p, st);
+    else if (in_bf16)
+        launch_write_t<true, false>(p, st);
+    else if (out_bf16)
+        launch_write_t<false, true>(p, st);
+    else
+        launch_write_t<false, false>(p, st);
+    return cudaGetLastError();
 }
 
 }  // namespace rf

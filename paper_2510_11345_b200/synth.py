@@ -206,15 +206,23 @@ class RankBatch:
         return int(self.lengths.sum())
 
 
-def make_rank_batch(wl: Workload, rank: int, world: int, seed: int = 42, prompts_per_rank: Optional[int] = None):
-    """Global batch = world x (prompts per rank) prompts; whole groups LPT-sharded to ranks."""
-    P = (prompts_per_rank or wl.prompts) * world
+def make_rank_batch(wl: Workload, rank: int, world: int, seed: int = 42, prompts_per_rank: Optional[int] = None,
+                    strong: bool = False):
+    """This rank's shard (whole groups, LPT on group token counts) of the global batch.
+
+    strong=False (weak scaling): global batch = world x (prompts per rank) prompts.
+    strong=True (strong scaling): the config's fixed global batch (``prompts_per_rank``
+    overrides the global prompt count) sharded over the world — the C5 sweep
+    (BASELINE.json configs[4], "batch evaluation may be data-parallel")."""
+    P = (prompts_per_rank or wl.prompts) * (1 if strong else world)
     G = wl.group
     lens = sequence_lengths(seed, P * G, wl.max_len)
     rew = group_rewards(seed, P, G)
     st = staleness(seed, P * G, wl.alpha)
     gt = lens.reshape(P, G).sum(axis=1)
     mine = lpt_shard(gt, world)[rank]
+    if not mine:
+        raise ValueError(f"rank {rank} of {world} owns no GRPO group ({P} groups)")
     idx = np.concatenate([np.arange(g * G, (g + 1) * G) for g in mine])
     return RankBatch(lengths=lens[idx], rewards=rew[idx], stale=st[idx], group=G,
                      global_tokens=int(lens.sum()), global_seqs=P * G)

@@ -111,6 +111,66 @@ def make_case(seed: int, *, T_seqs: int, G: int, V: int, max_len: int, mapping: 
                 group_offsets=go)
 
 
+def make_pool_case(seed: int, *, V: int, R: int, T_min: int, G: int = 8, max_len: int = 64, scale: float = 2.0,
+                   stale: float = 0.2, alpha: int = 2, round_bf16: bool = True, kl: bool = False,
+                   mapping: str = "A", draws: int = 16) -> Case:
+    """A batch shaped like the benchmark's DeviceWorkload (synth.py): a pool of R
+    logits rows and at least T_min tokens whose rows wrap the pool
+    (row_of_token[t] = t mod R), each token drawn from its row's softmax (draw
+    (t div R) mod ``draws`` of the row).  mapping "B": every sequence reads one pool
+    row (its context).  Sizes are chosen so a persistent kernel gets many rows per
+    CTA / cluster while the fp64 oracle stays at seconds."""
+    rng = np.random.default_rng(seed)
+    lens = []
+    while sum(lens) < T_min or len(lens) % G:
+        lens.append(int(min(max_len, max(1, np.ceil(np.exp(rng.normal(np.log(max(max_len / 8, 1)), 1.0)))))))
+    lens = np.array(lens, dtype=np.int64)
+    N = len(lens)
+    offs = np.zeros(N + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lens)
+    T = int(offs[-1])
+    logits = rng.normal(0.0, scale, (R, V))
+    if round_bf16:
+        logits = bf16_round(logits)
+    lp_all = log_softmax_rows(logits)
+    p_all = np.exp(lp_all)
+    tab = np.stack([rng.choice(V, size=draws, p=p_all[r] / p_all[r].sum()) for r in range(R)]).astype(np.int32)
+    del p_all
+    t = np.arange(T)
+    if mapping == "A":
+        rows = (t % R).astype(np.int32)
+        tok = tab[rows, (t // R) % draws]
+    else:
+        seq = np.repeat(np.arange(N), lens)
+        rows = (seq % R).astype(np.int32)
+        tok = tab[rows, (t - offs[seq]) % draws]
+    lp = lp_all[rows, tok]
+    s = rng.integers(0, alpha + 1, N)
+    delta = rng.normal(0.0, 1.0, T) * stale * np.sqrt(np.repeat(s, lens))
+    behavior = lp - delta
+    prox = lp - delta / 2
+    eng = behavior - rng.normal(0.0, 0.01, T)
+    ngroups = N // G
+    go = np.arange(ngroups + 1, dtype=np.int64) * G
+    p_prompt = rng.uniform(0, 1, ngroups)
+    rewards = (rng.uniform(0, 1, N) < np.repeat(p_prompt, G)).astype(np.float64)
+    adv = np.zeros(N)
+    for gi in range(ngroups):
+        r = rewards[go[gi]:go[gi + 1]]
+        mean = r.sum() / len(r)
+        sd = np.sqrt(((r - mean) ** 2).sum() / len(r))
+        if sd >= 1e-8:
+            adv[go[gi]:go[gi + 1]] = (r - mean) / sd
+    ref = None
+    if kl:
+        ref = logits + rng.normal(0.0, 0.3, logits.shape)
+        if round_bf16:
+            ref = bf16_round(ref)
+    return Case(logits=logits, token_ids=tok.astype(np.int32), seq_offsets=offs, advantages=adv,
+                behavior_logp=behavior, row_of_token=rows, prox_logp=prox, engine_logp=eng, ref_logits=ref,
+                rewards=rewards, group_offsets=go)
+
+
 def config(variant: str, **kw) -> LossConfig:
     c = LossConfig(variant=LossVariant[variant], **{k: v for k, v in kw.items() if k != "aggregation"})
     if "aggregation" in kw:

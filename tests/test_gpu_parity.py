@@ -310,10 +310,11 @@ print("arm ok")
 """
 
 
-@pytest.mark.parametrize("env,kl", [({"RF_KL_GX": "0"}, True), ({"RF_SP_STATS": "ring"}, False)])
+@pytest.mark.parametrize("env,kl", [({"RF_KL_GX": "0"}, True)])
 def test_ab_arms_parity(env, kl):
-    """The A/B arms behind environment knobs (read once per process, so each runs in a
-    subprocess): hardware-cluster exact KL, lag-kernel stats pass of sequence_product."""
+    """The exact-KL hardware-cluster kernel (the fallback when the cooperative CTA-group
+    launch cannot place every CTA; selected with RF_KL_GX=0, read once per process, so
+    it runs in a subprocess)."""
     import os
     import subprocess
     import sys

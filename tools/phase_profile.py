@@ -43,7 +43,7 @@ names = ["cons.full_wait", "cons.stream", "cons.park", "cons.coef_wait", "cons.w
          "scal.post_to_k", "scal.post.lse", "scal.post.token_post"]
 ncta = 148
 print(f"launch {ms:.3f} ms for {op.chunk} tokens -> {op.chunk * 4 * wl.vocab / ms / 1e6:.1f} GB/s")
-cons_warps = ncta * int(os.environ.get("RF_LAG_WARPS", "12"))
+cons_warps = ncta * 12
 for i, n in enumerate(names):
     div = cons_warps if n.startswith("cons") else (ncta * 2 if n.startswith("scal") else ncta)
     print(f"{n:18s} {buf[i] / div / 1e3:10.1f} kcycles per warp   ({buf[i] / max(buf[5 if n.startswith('cons') else (9 if n.startswith('scal') else 11)], 1) * 100:5.1f}%)")

@@ -1,7 +1,7 @@
 #!/bin/bash
 # All BASELINE.json configs on one GPU (run on the GPU box): gpurun_out/sweep_<name>.log
 mkdir -p gpurun_out
-run() { name=$1; shift; timeout 900 python bench.py --no-e2e --no-cpu-baseline "$@" > gpurun_out/sweep_$name.log 2>&1; echo "$name rc=$?" >> gpurun_out/sweep_rc.log; }
+run() { name=$1; shift; timeout 900 python bench.py --no-e2e --no-cpu-baseline --check 64 "$@" > gpurun_out/sweep_$name.log 2>&1; echo "$name rc=$?" >> gpurun_out/sweep_rc.log; }
 rm -f gpurun_out/sweep_rc.log
 run c1 --workload c1 --steps 5 --warmup 3
 run c2 --workload c2 --steps 5 --warmup 3
