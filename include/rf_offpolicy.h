@@ -95,8 +95,12 @@ typedef enum {
 } rf_status;
 
 /* Bits of *device_status. */
-#define RF_DEVSTAT_NONFINITE_RATIO 0x1
-#define RF_DEVSTAT_TOKEN_OUT_OF_RANGE 0x2
+#define RF_DEVSTAT_NONFINITE_RATIO 0x1    /* exp(lp - b) not finite (losses.cpp:205,267) */
+#define RF_DEVSTAT_TOKEN_OUT_OF_RANGE 0x2 /* token id outside [0, V) (UB in the reference) */
+#define RF_DEVSTAT_GROUP_TOO_SMALL 0x4    /* rf_grpo_advantages: a group of < 2 (losses.cpp:42);
+                                             its advantages are zeroed */
+#define RF_DEVSTAT_EMPTY_TRAJECTORY 0x8   /* a sequence with no tokens (losses.cpp:157), checked
+                                             over the sequences each call spans */
 
 /* Per-token flag bits (token_flags[t]).  Bit-exact contract vs the reference's
  * branch conditions (losses.cpp:275-312):
@@ -213,6 +217,17 @@ rf_status rf_loss_and_grad(const rf_loss_config* cfg, const rf_batch* batch, rf_
                            void* stream);
 rf_status rf_loss_and_grad_ex(const rf_loss_config* cfg, const rf_batch* batch, rf_outputs* outputs,
                               void* stream, int32_t kernel);
+
+/* Segmented row sums for the reference-layout gradient: for every segment s,
+ *   out[s * out_stride + v] = sum over i in [seg_offsets[s], seg_offsets[s+1]) of
+ *                             rows[seg_rows[i] * row_stride + v]      (v < width)
+ * in fp64, in index order (deterministic).  With rows = per-token dlogits and one
+ * segment per context listing that context's tokens, this is LossResult.grad
+ * (LogProbGrad's per-context accumulation, losses.cpp:87-115).  Device pointers,
+ * stream-ordered; rows bf16 or f32; at most 65,535 segments per call. */
+rf_status rf_rows_segment_sum(const void* rows, int32_t rows_dtype, int64_t row_stride, const int64_t* seg_offsets,
+                              const int32_t* seg_rows, int64_t num_segments, int32_t width, double* out,
+                              int64_t out_stride, void* stream);
 
 /* Number of CUDA kernel launches the last rf_loss_and_grad* call made on this
  * thread (for benchmark accounting). */

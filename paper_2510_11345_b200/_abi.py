@@ -46,6 +46,8 @@ RF_ERR_CUDA = 19
 
 RF_DEVSTAT_NONFINITE_RATIO = 0x1
 RF_DEVSTAT_TOKEN_OUT_OF_RANGE = 0x2
+RF_DEVSTAT_GROUP_TOO_SMALL = 0x4
+RF_DEVSTAT_EMPTY_TRAJECTORY = 0x8
 
 RF_FLAG_CLIPPED = 0x01
 RF_FLAG_TOPR_POS = 0x02
@@ -144,6 +146,7 @@ EXPORTED_SYMBOLS = (
     "rf_lmhead_lse",
     "rf_lmhead_dlogits",
     "rf_token_loss_from_stats",
+    "rf_rows_segment_sum",
 )
 
 _lib = None
@@ -196,6 +199,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rf_lmhead_dlogits.restype = _i32
     lib.rf_token_loss_from_stats.argtypes = [P(rf_loss_config), P(rf_batch), _p, _p, P(rf_outputs), _p]
     lib.rf_token_loss_from_stats.restype = _i32
+    lib.rf_rows_segment_sum.argtypes = [_p, _i32, _i64, _p, _p, _i64, _i32, _p, _i64, _p]
+    lib.rf_rows_segment_sum.restype = _i32
     lib.rf_debug_counters.argtypes = [_p, _i32, _i32]
     lib.rf_debug_counters.restype = _i32
     _lib = lib

@@ -161,6 +161,7 @@ int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t s
 // exact KL: CTA groups exchanging through L2 (rf_ring_kl.cu GX) fill all 148 SMs
 // where 4-CTA hardware clusters place on 132; RF_KL_GX=0 selects the clusters (A/B).
 constexpr int kKlMaxGroups = 256;
+constexpr size_t kKlSlotBytes = 32 * 40;  // per group: [4 row slots][8 ranks] x sizeof(XSlotG)
 bool kl_groups_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("RF_KL_GX");
@@ -192,7 +193,7 @@ WsLayout ws_layout(const rf_loss_config* c, const rf_batch* b, void* base) {
         return static_cast<double*>(r);
     };
     w.partials = take(static_cast<size_t>(partial_rows(b)) * RF_NUM_SCALARS * sizeof(double));
-    if (c->variant == RF_GRPO && c->kl_weight > 0.0) w.xch = take(kKlMaxGroups * 32 * 40);
+    if (c->variant == RF_GRPO && c->kl_weight > 0.0) w.xch = take(kKlMaxGroups * kKlSlotBytes);
     if (c->aggregation == RF_SEQUENCE_PRODUCT) {
         const size_t T = static_cast<size_t>(b->num_tokens);
         w.lse = take(T * 8);
@@ -466,14 +467,17 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             p.nslots = g.nslots;
             int maxc = ring_clusters(ib, ob, g.kind, g.ncw, g.nvt, g.cs, g.smem);
             if (g.kind == 3 && g.cs > 1 && kl_groups_enabled()) {
-                static std::atomic<unsigned long long> epoch{0};
                 int dev = 0, sms = 148;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
                 maxc = std::min(kKlMaxGroups, sms / g.cs);
                 p.vcs = g.cs;
                 p.xch = ws.xch;
-                p.xch_epoch = ++epoch;
+                // The groups' L2 exchange slots carry sequence words row + 1: zero them in
+                // stream order before every launch, so no slot of an earlier launch (or an
+                // earlier replay of a captured CUDA graph) can match.
+                if (cudaMemsetAsync(ws.xch, 0, static_cast<size_t>(kKlMaxGroups) * kKlSlotBytes, s) != cudaSuccess)
+                    return RF_ERR_CUDA;
             }
             int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
             cudaError_t e = g.kind == 3 ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
@@ -496,7 +500,9 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
         }
         g_last_launches = 1;
     }
-    if (rf::launch_finalize(ws.partials, nparts, o->scalars, s) != cudaSuccess) return RF_ERR_CUDA;
+    if (rf::launch_finalize(ws.partials, nparts, o->scalars, b->seq_of_token, b->seq_offsets, b->num_tokens,
+                            b->num_seqs, o->device_status, s) != cudaSuccess)
+        return RF_ERR_CUDA;
     g_last_launches += 1;
     return RF_OK;
 }
@@ -584,10 +590,24 @@ rf_status rf_token_loss_from_stats(const rf_loss_config* c, const rf_batch* b, c
     p.partials = ws.partials;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (rf::launch_token_loss(p, lse, x_tok, s) != cudaSuccess) return RF_ERR_CUDA;
-    if (rf::launch_finalize(ws.partials, (b->num_tokens + 255) / 256, o->scalars, s) != cudaSuccess)
+    if (rf::launch_finalize(ws.partials, (b->num_tokens + 255) / 256, o->scalars, b->seq_of_token, b->seq_offsets,
+                            b->num_tokens, b->num_seqs, o->device_status, s) != cudaSuccess)
         return RF_ERR_CUDA;
     g_last_launches = 2;
     return RF_OK;
+}
+
+rf_status rf_rows_segment_sum(const void* rows, int32_t rows_dtype, int64_t row_stride, const int64_t* seg_offsets,
+                              const int32_t* seg_rows, int64_t num_segments, int32_t width, double* out,
+                              int64_t out_stride, void* stream) {
+    if (!rows || !seg_offsets || !seg_rows || !out) return RF_ERR_INVALID_ARGUMENT;
+    if (rows_dtype != RF_DTYPE_BF16 && rows_dtype != RF_DTYPE_F32) return RF_ERR_INVALID_ARGUMENT;
+    if (num_segments <= 0 || width <= 0 || row_stride < width || out_stride < width) return RF_ERR_INVALID_ARGUMENT;
+    if (num_segments > 65535) return RF_ERR_UNSUPPORTED_LAYOUT;
+    g_last_launches = 1;
+    return check_cuda(rf::launch_rows_segment_sum(rows, rows_dtype == RF_DTYPE_BF16, row_stride, seg_offsets, seg_rows,
+                                                  num_segments, width, out, out_stride,
+                                                  static_cast<cudaStream_t>(stream)));
 }
 
 rf_status rf_loss_and_grad(const rf_loss_config* c, const rf_batch* b, rf_outputs* o, void* stream) {

@@ -61,7 +61,6 @@ struct KParams {
     unsigned long long* dbg;  // optional per-phase cycle counters (RF_DEBUG_COUNTERS), else nullptr
     // exact-KL kernel with CTA groups exchanging through L2 instead of a hardware cluster
     void* xch;                 // [groups][4 row slots][8 ranks] exchange slots (workspace)
-    unsigned long long xch_epoch;  // launch epoch in the high half of the slot sequence words
     int32_t vcs;               // CTAs per group (0 = hardware cluster)
 };
 

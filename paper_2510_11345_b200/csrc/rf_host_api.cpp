@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "rf_offpolicy.h"
@@ -25,9 +27,32 @@ struct Chunk {
     int64_t s0, s1;  // sequence range (sequence_product: the call's sub-view)
 };
 
+// The host API's own stream-ordered memory pool per device, with its memory kept
+// mapped between calls (a release threshold of 0 would return it to the OS at every
+// synchronisation).  Private, so the process's default pool (e.g. PyTorch's
+// cudaMallocAsync backend) keeps its own trimming behaviour.
+cudaMemPool_t host_api_pool(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(device);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[device] = pool;
+    return pool;
+}
+
 struct DevBuf {
     void* p = nullptr;
-    cudaError_t alloc(size_t n, cudaStream_t s) { return n ? cudaMallocAsync(&p, n, s) : cudaSuccess; }
+    cudaMemPool_t pool = nullptr;
+    cudaError_t alloc(size_t n, cudaStream_t s) { return n ? cudaMallocFromPoolAsync(&p, n, pool, s) : cudaSuccess; }
     void release(cudaStream_t s) {
         if (p) cudaFreeAsync(p, s);
         p = nullptr;
@@ -88,15 +113,8 @@ extern "C" rf_status rf_loss_and_grad_host(const rf_loss_config* c, const rf_bat
     const size_t row_bytes = static_cast<size_t>(hb->logits_row_stride) * les;
     const size_t drow_bytes = static_cast<size_t>(ho->dlogits_row_stride) * des;
 
-    // Keep the stream-ordered pool's memory mapped between calls (the default
-    // release threshold of 0 returns it to the OS at every synchronisation).
-    {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    }
+    cudaMemPool_t pool = host_api_pool(device);
+    if (!pool) return RF_ERR_CUDA;
     cudaStream_t s_h2d, s_cmp, s_d2h;
     cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&s_cmp, cudaStreamNonBlocking);
@@ -113,6 +131,7 @@ extern "C" rf_status rf_loss_and_grad_host(const rf_loss_config* c, const rf_bat
         d_coef, d_loss, d_flags, d_scal, d_status, d_ws;
     rf_status rc = RF_OK;
     auto A = [&](DevBuf& b, size_t n) {
+        b.pool = pool;
         if (rc == RF_OK && b.alloc(n, s_cmp) != cudaSuccess) rc = RF_ERR_CUDA;
     };
     A(d_tok, T * 4);
@@ -150,7 +169,16 @@ extern "C" rf_status rf_loss_and_grad_host(const rf_loss_config* c, const rf_bat
             rc = RF_ERR_CUDA;
     };
     H2D(d_tok.p, hb->token_ids, T * 4, s_cmp);
-    H2D(d_seqof.p, hb->seq_of_token, T * 4, s_cmp);
+    // sequence_product calls see a sub-view of the sequence arrays, so each chunk's
+    // seq_of_token is rebased to its first sequence (host copy, uploaded once)
+    std::vector<int32_t> rebased;
+    if (seqprod) {
+        rebased.resize(static_cast<size_t>(T));
+        for (const Chunk& ch : chunks)
+            for (int64_t t = ch.t0; t < ch.t1; ++t)
+                rebased[static_cast<size_t>(t)] = hb->seq_of_token[t] - static_cast<int32_t>(ch.s0);
+    }
+    H2D(d_seqof.p, seqprod ? rebased.data() : static_cast<const void*>(hb->seq_of_token), T * 4, s_cmp);
     H2D(d_offs.p, hb->seq_offsets, (N + 1) * 8, s_cmp);
     H2D(d_adv.p, hb->advantages, N * 8, s_cmp);
     H2D(d_b.p, hb->behavior_logp, T * lps, s_cmp);
@@ -223,18 +251,6 @@ extern "C" rf_status rf_loss_and_grad_host(const rf_loss_config* c, const rf_bat
         dout.device_status = static_cast<int32_t*>(d_status.p);
         dout.workspace = d_ws.p;
         dout.workspace_bytes = wsb;
-        if (seqprod) {
-            // seq_of_token of this chunk is relative to the sub-view: the caller's
-            // global indices are rebased on the host copy.
-            std::vector<int32_t> rebased(static_cast<size_t>(n));
-            for (int64_t t = 0; t < n; ++t)
-                rebased[static_cast<size_t>(t)] = hb->seq_of_token[ch.t0 + t] - static_cast<int32_t>(ch.s0);
-            int32_t* dst = static_cast<int32_t*>(d_seqof.p) + ch.t0;
-            if (cudaMemcpyAsync(dst, rebased.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, s_cmp) !=
-                cudaSuccess)
-                rc = RF_ERR_CUDA;
-            cudaStreamSynchronize(s_cmp);  // rebased is a stack buffer
-        }
         const rf_status ks = rf_loss_and_grad(c, &db, &dout, s_cmp);
         if (ks != RF_OK) rc = ks;
         cudaEventRecord(ev_cmp[bi], s_cmp);
@@ -281,5 +297,6 @@ extern "C" rf_status rf_loss_and_grad_host(const rf_loss_config* c, const rf_bat
     cudaStreamDestroy(s_d2h);
     if (rc == RF_OK && (dev_status & RF_DEVSTAT_NONFINITE_RATIO)) rc = RF_ERR_NONFINITE_RATIO;  // losses.cpp:267
     if (rc == RF_OK && (dev_status & RF_DEVSTAT_TOKEN_OUT_OF_RANGE)) rc = RF_ERR_TOKEN_OUT_OF_RANGE;
+    if (rc == RF_OK && (dev_status & RF_DEVSTAT_EMPTY_TRAJECTORY)) rc = RF_ERR_EMPTY_TRAJECTORY;
     return rc;
 }

@@ -27,8 +27,10 @@ __global__ void grpo_group_kernel(const double* __restrict__ rewards, const int6
     const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g >= num_groups) return;
     const int64_t b = group_offsets[g], e = group_offsets[g + 1];
-    if (e - b < 2) {  // losses.cpp:42 throws; host validated, flag defensively
-        atomicOr(status, RF_DEVSTAT_TOKEN_OUT_OF_RANGE);
+    if (e - b < 2) {  // losses.cpp:42 throws: flag it, and leave defined outputs behind
+        atomicOr(status, RF_DEVSTAT_GROUP_TOO_SMALL);
+        degenerate[g] = 0;
+        for (int64_t i = b; i < e; ++i) adv[i] = 0.0;
         return;
     }
     const double n = static_cast<double>(e - b);
@@ -411,8 +413,26 @@ cudaError_t launch_token_loss(const KParams& p, const float* lse, const float* x
 // ===========================================================================
 // K3: scalars[j] += sum_i partials[i][j] in a fixed order (deterministic).
 // ===========================================================================
-__global__ void finalize_kernel(const double* __restrict__ partials, int64_t n, double* __restrict__ scalars) {
+// K3 also carries the device-side empty-trajectory check (losses.cpp:157 throws on
+// an empty trajectory; the host API validates it on the host): this call's tokens
+// span sequences [lo, hi] = [seq_of_token[0], seq_of_token[T-1]].  Every empty
+// sequence i is then seen by some call: strictly inside [lo, hi], as lo - 1 of the
+// call whose first token starts the next non-empty sequence, or as hi + 1 of the
+// call holding the batch's last token (trailing).  O(hi - lo) loads per call.
+__global__ void finalize_kernel(const double* __restrict__ partials, int64_t n, double* __restrict__ scalars,
+                                const int32_t* __restrict__ seq_of_token, const int64_t* __restrict__ seq_offsets,
+                                int64_t num_tokens, int64_t num_seqs, int32_t* __restrict__ status) {
     __shared__ double sh[256];
+    if (seq_of_token != nullptr && num_tokens > 0) {
+        const int64_t lo = seq_of_token[0], hi = seq_of_token[num_tokens - 1];
+        bool empty = false;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += 256) empty |= seq_offsets[i + 1] <= seq_offsets[i];
+        if (threadIdx.x == 0) {
+            if (lo > 0 && lo <= num_seqs) empty |= seq_offsets[lo] <= seq_offsets[lo - 1];
+            if (hi + 1 < num_seqs) empty |= seq_offsets[hi + 2] <= seq_offsets[hi + 1];
+        }
+        if (empty) atomicOr(status, RF_DEVSTAT_EMPTY_TRAJECTORY);
+    }
     for (int j = 0; j < RF_NUM_SCALARS; ++j) {
         double a = 0.0;
         for (int64_t i = threadIdx.x; i < n; i += 256) a += partials[i * RF_NUM_SCALARS + j];
@@ -425,6 +445,26 @@ __global__ void finalize_kernel(const double* __restrict__ partials, int64_t n, 
         if (threadIdx.x == 0) scalars[j] += sh[0];
         __syncthreads();
     }
+}
+
+// ===========================================================================
+// Segmented row sums (rf_rows_segment_sum): out[s][v] = Σ_{i in segment s}
+// rows[seg_rows[i]][v] in fp64, index order (deterministic).  One thread per
+// column, coalesced across a warp; grid (column blocks, segments).  The reference
+// binding folds per-token dlogits into LossResult.grad with it (LogProbGrad's
+// per-context accumulation, losses.cpp:87-115).
+// ===========================================================================
+template <typename T>
+__global__ void rows_segment_sum_kernel(const T* __restrict__ rows, int64_t row_stride,
+                                        const int64_t* __restrict__ seg_offsets, const int32_t* __restrict__ seg_rows,
+                                        int32_t width, double* __restrict__ out, int64_t out_stride) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t s = blockIdx.y;
+    if (v >= width) return;
+    double acc = 0.0;
+    for (int64_t i = seg_offsets[s]; i < seg_offsets[s + 1]; ++i)
+        acc += static_cast<double>(static_cast<float>(rows[static_cast<int64_t>(seg_rows[i]) * row_stride + v]));
+    out[s * out_stride + v] = acc;
 }
 
 // ===========================================================================
@@ -442,8 +482,23 @@ cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, cudaStream_t st) {
-    finalize_kernel<<<1, 256, 0, st>>>(partials, n, scalars);
+cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, const int32_t* seq_of_token,
+                            const int64_t* seq_offsets, int64_t num_tokens, int64_t num_seqs, int32_t* status,
+                            cudaStream_t st) {
+    finalize_kernel<<<1, 256, 0, st>>>(partials, n, scalars, seq_of_token, seq_offsets, num_tokens, num_seqs, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_segment_sum(const void* rows, bool bf16, int64_t row_stride, const int64_t* seg_offsets,
+                                    const int32_t* seg_rows, int64_t num_segments, int32_t width, double* out,
+                                    int64_t out_stride, cudaStream_t st) {
+    const dim3 grid(static_cast<unsigned>((width + 255) / 256), static_cast<unsigned>(num_segments));
+    if (bf16)
+        rows_segment_sum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(rows), row_stride,
+                                                                     seg_offsets, seg_rows, width, out, out_stride);
+    else
+        rows_segment_sum_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(rows), row_stride, seg_offsets,
+                                                             seg_rows, width, out, out_stride);
     return cudaGetLastError();
 }
 

@@ -55,7 +55,13 @@ cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, c
 cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st);
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st);
 cudaError_t launch_token_loss(const KParams& p, const float* lse, const float* xtok, cudaStream_t st);
-cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, cudaStream_t st);
+// K3: scalar reduce + the empty-trajectory check over the sequences this call spans
+cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, const int32_t* seq_of_token,
+                            const int64_t* seq_offsets, int64_t num_tokens, int64_t num_seqs, int32_t* status,
+                            cudaStream_t st);
+cudaError_t launch_rows_segment_sum(const void* rows, bool bf16, int64_t row_stride, const int64_t* seg_offsets,
+                                    const int32_t* seg_rows, int64_t num_segments, int32_t width, double* out,
+                                    int64_t out_stride, cudaStream_t st);
 cudaError_t launch_grpo(const double* rewards, const int64_t* group_offsets, int64_t num_groups, double* adv,
                         uint8_t* degenerate, int32_t* status, cudaStream_t st);
 

@@ -133,7 +133,7 @@ __device__ __forceinline__ float vmax_row(const uint4* r, int n) {
 struct XSlotG {  // [group][row % 4][sender rank]
     double S, T, Sy;
     float M, My;
-    unsigned long long seq;  // (launch epoch << 32) | (row_iter + 1)
+    unsigned long long seq;  // row_iter + 1 (the slots are zeroed before every launch)
 };
 
 template <bool OUT_BF16, int NCW, int NVT, bool GX>
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     st_relaxed_gpu_f64(&mine->Sy, Syw);
                     st_relaxed_gpu_f32(&mine->M, Mw);
                     st_relaxed_gpu_f32(&mine->My, Myw);
-                    const unsigned long long want = (p.xch_epoch << 32) | (row_iter + 1);
+                    const unsigned long long want = row_iter + 1;
                     st_release_gpu_u64(&mine->seq, want);
                     float Mq[8], Myq[8];
                     double Sq[8], Tq[8], Syq[8];

@@ -265,10 +265,13 @@ def grpo_advantages(rewards: torch.Tensor, group_offsets: torch.Tensor, stream=N
     """K1 — rlsim::grpo_advantages (losses.cpp:41-60) over CSR groups on the GPU.
 
     Returns (advantages f64 [N], degenerate uint8 [G]).  Bit-identical to the
-    reference.  Raises InvalidArgument for a group smaller than 2 (``validate``
-    reads the offsets on the host; a training loop validates its batch layout
-    once and passes ``validate=False`` plus preallocated ``out=(adv, deg,
-    status)`` to keep the step free of host syncs and allocations).
+    reference.  Raises InvalidArgument for a group smaller than 2, as the reference
+    does (losses.cpp:42): ``validate`` checks the offsets on the host before the
+    launch and the device status after it.  A training loop validates its batch
+    layout once and passes ``validate=False`` plus preallocated ``out=(adv, deg,
+    status)`` to keep the step free of host syncs and allocations; the kernel then
+    ORs RF_DEVSTAT_GROUP_TOO_SMALL into ``status`` (and zeroes that group's
+    advantages) for the caller to read later.
     """
     G = int(group_offsets.numel() - 1)
     if G <= 0:
@@ -278,12 +281,18 @@ def grpo_advantages(rewards: torch.Tensor, group_offsets: torch.Tensor, stream=N
         if bool((sizes < 2).any()):
             raise InvalidArgument("grpo_advantages: group size must be >= 2")
     dev = rewards.device
-    if out is not None:
-        adv, deg, status = out
+    if stream is not None:
+        ctx = torch.cuda.stream(stream)
     else:
-        adv = torch.empty_like(rewards, dtype=torch.float64)
-        deg = torch.empty(G, dtype=torch.uint8, device=dev)
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        import contextlib
+        ctx = contextlib.nullcontext()
+    with ctx:  # temporaries belong to the launching stream (caching-allocator ordering)
+        if out is not None:
+            adv, deg, status = out
+        else:
+            adv = torch.empty_like(rewards, dtype=torch.float64)
+            deg = torch.empty(G, dtype=torch.uint8, device=dev)
+            status = torch.zeros(1, dtype=torch.int32, device=dev)
     b = rf_batch()
     b.num_groups = G
     b.num_seqs = int(rewards.numel())
@@ -294,6 +303,8 @@ def grpo_advantages(rewards: torch.Tensor, group_offsets: torch.Tensor, stream=N
     o.group_degenerate = deg.data_ptr()
     o.device_status = status.data_ptr()
     _raise_for(_lib().rf_grpo_advantages(ctypes.byref(b), ctypes.byref(o), _stream_handle(stream)))
+    if validate and int(status.item()) & _abi.RF_DEVSTAT_GROUP_TOO_SMALL:
+        raise InvalidArgument("grpo_advantages: group size must be >= 2")
     return adv, deg
 
 
@@ -382,7 +393,11 @@ def loss_and_grad(config: LossConfig, batch: PackedBatch, *, dlogits_dtype=torch
     InvalidArgument on a non-finite ratio, as the reference does
     (losses.cpp:205,267).
     """
-    op = OffPolicyLoss(config, batch, dlogits_dtype=dlogits_dtype, want_dlogits=want_dlogits, kernel=kernel)
+    if stream is not None:
+        with torch.cuda.stream(stream):  # outputs + workspace belong to the launching stream
+            op = OffPolicyLoss(config, batch, dlogits_dtype=dlogits_dtype, want_dlogits=want_dlogits, kernel=kernel)
+    else:
+        op = OffPolicyLoss(config, batch, dlogits_dtype=dlogits_dtype, want_dlogits=want_dlogits, kernel=kernel)
     op.zero(stream)
     op.run(batch, 0, batch.num_tokens, stream)
     res = LossResult(scalars=op.scalars, dlogits=op.dlogits, token_logp=op.token_logp,
@@ -395,6 +410,8 @@ def loss_and_grad(config: LossConfig, batch: PackedBatch, *, dlogits_dtype=torch
             raise InvalidArgument("loss_and_grad: non-finite ratio")
         if st & _abi.RF_DEVSTAT_TOKEN_OUT_OF_RANGE:
             raise InvalidArgument(status_string(_abi.RF_ERR_TOKEN_OUT_OF_RANGE))
+        if st & _abi.RF_DEVSTAT_EMPTY_TRAJECTORY:
+            raise InvalidArgument("loss_and_grad: empty trajectory")
     return res
 
 
