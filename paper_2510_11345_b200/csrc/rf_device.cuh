@@ -71,6 +71,20 @@ struct KParams {
 #endif
 constexpr bool kPhaseCounters = RF_PHASE_COUNTERS != 0;
 
+// Protocol-checked build (make checked -> librf_offpolicy_checked.so, load with
+// RF_LIB_VARIANT=checked): every cross-warp handoff of the persistent kernels
+// carries the token index it belongs to and the receiver traps on a mismatch
+// (a partial or coefficient taken from the wrong row, a stale exchange slot, a
+// ring phase slip), plus bounds asserts on the computed dlogits vector indices.
+// compute-sanitizer is not available on this GPU pool; this build is its stand-in.
+#ifndef RF_CHECKED
+#define RF_CHECKED 0
+#endif
+constexpr bool kChecked = RF_CHECKED != 0;
+__device__ __forceinline__ void rf_check(bool ok) {
+    if (RF_CHECKED && !ok) __trap();
+}
+
 // Debug phase timer: accumulates clock64 deltas into a per-thread slot array.
 struct PhaseClock {
     long long t;

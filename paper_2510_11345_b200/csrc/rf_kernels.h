@@ -26,13 +26,15 @@ __host__ __device__ constexpr unsigned lag_tmem_cols(int ncw) { return (512u / (
 // vectors per thread per TMA chunk of the lag kernels: 5 (30 KB chunks at 12
 // consumer warps, measured best of {2,3,4,5,7,9,13}) for the long rows, 2 for NVT = 4
 __host__ __device__ constexpr int lag_vpc(int nvt) { return nvt >= 9 ? 5 : 2; }
-constexpr size_t kRingLagTailBytes = 1088;  // exchange / reduce / broadcast words
+// exchange / reduce / broadcast words (+ the checked build's row tags at 1088: [2][16] + [2])
+constexpr size_t kRingLagTailBytes = RF_CHECKED ? 1088 + 32 * 8 + 16 : 1088;
 constexpr size_t kRingLagBarrierBytes = 48;
 
 // Exact-KL lag kernel (rf_ring_kl.cu): policy and reference rows co-resident,
 // 12 consumer warps, bf16 logits; NVT = 13 covers a quarter Qwen3 row (4-CTA cluster).
 constexpr int kRingNvtKL[3] = {4, 10, 13};  // 13: 4-CTA groups at V=151,936 (5-CTA groups at NVT 10 measured -6%)
-constexpr size_t kRingKLTailBytes = 2176;  // [4][8] 40-byte exchange slots + 5 x [2][NCW] partials + broadcast
+// [4][8] 40-byte exchange slots + 5 x [2][NCW] partials + broadcast (+ checked-build row tags)
+constexpr size_t kRingKLTailBytes = RF_CHECKED ? 2176 + 2 * 16 * 8 + 16 : 2176;
 cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int nclusters, size_t smem,
                            cudaStream_t st);
 cudaError_t ring_kl_max_clusters(bool out_bf16, int nvt, int cs, size_t smem, int* out);

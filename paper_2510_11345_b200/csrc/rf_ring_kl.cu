@@ -178,6 +178,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
     };
     Bcast* bcs = reinterpret_cast<Bcast*>(tail + 1280 + 64 * NCW);  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bcs + 2);
+    int64_t* red_tag = reinterpret_cast<int64_t*>(tail + 2176);  // [2][NCW] checked build: row of each partial
+    int64_t* bc_tag = red_tag + 32;                               // [2] checked build: row of each broadcast
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -264,6 +266,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
                 support_wait(bar_red + 8 * par, ph);
+                if (kChecked)
+                    for (int w = 0; w < NCW; ++w) rf_check(red_tag[par * NCW + w] == t);
                 // CTA partials, warp order
                 float Mw = -CUDART_INF_F, Myw = -CUDART_INF_F;
                 for (int w = 0; w < NCW; ++w) {
@@ -400,6 +404,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     bc->tok_val = 0.0;
                     bc->tok = -1;
                 }
+                if (kChecked) bc_tag[par] = t;
                 mbar_arrive(bar_bc + 8 * par);
                 const double lseq = kLn2 * (Myc + log2(Syc));
                 const double klv = D - lse + lseq;  // Σ p_v (lp_v - lq_v)
@@ -446,7 +451,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         const size_t thr_off = static_cast<size_t>(slice_begin + tid) * EPV * OES;
 
         // copy-in (parking the previous row's e and d chunk by chunk), max, sweep, reduce
-        auto stream_row = [&](uint32_t row_iter, bool park_prev) -> float {
+        auto stream_row = [&](int64_t t_row, uint32_t row_iter, bool park_prev) -> float {
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
                 if (park_prev) {
@@ -530,6 +535,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 redS[par * NCW + warp] = sw;
                 redT[par * NCW + warp] = tw;
                 redSy[par * NCW + warp] = syw;
+                if (kChecked) red_tag[par * NCW + warp] = t_row;
                 mbar_arrive(bar_red + 8 * par);
             }
             return C;
@@ -538,6 +544,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         auto write_row = [&](int64_t t, uint32_t row_iter, float C) {
             const uint32_t par = row_iter & 1;
             cons_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
+            if (kChecked) rf_check(bc_tag[par] == t);
             const Bcast* bc = bcs + par;
             const float f = ex2_approx(C - bc->lseL);
             const float A = f * bc->A, B = f * bc->B;
@@ -593,7 +600,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         uint32_t it = 0;
         int64_t t = cid;
         float C = 0.f;
-        if (t < p.T) C = stream_row(0, false);
+        if (t < p.T) C = stream_row(t, 0, false);
         while (t < p.T) {
             const int64_t tn = t + ncl;
             if (tn >= p.T) {  // last row: park it whole
@@ -604,7 +611,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 }
             }
             float Cn = 0.f;
-            if (tn < p.T) Cn = stream_row(it + 1, true);
+            if (tn < p.T) Cn = stream_row(tn, it + 1, true);
             tmem_wait_st();
             write_row(t, it, C);
             C = Cn;

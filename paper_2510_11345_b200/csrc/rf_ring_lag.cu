@@ -77,6 +77,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
     };
     Bcast* bcs = reinterpret_cast<Bcast*>(tail + 512 + 24 * NCW + ((24 * NCW) % 8 ? 4 : 0));  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bcs + 2);
+    int64_t* red_tag = reinterpret_cast<int64_t*>(tail + 1088);  // [2][NCW] checked build: row of each partial
+    int64_t* bc_tag = red_tag + 32;                               // [2] checked build: row of each broadcast
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -185,6 +187,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
                 support_wait(bar_red + 8 * par, ph);
                 if (kPhaseCounters && p.dbg) pc.lap(d_red);
+                if (kChecked)
+                    for (int w = 0; w < NCW; ++w) rf_check(red_tag[par * NCW + w] == t);
                 // combine the consumer warps' partials, sequential in warp order
                 float Mw = -CUDART_INF_F;
                 for (int w = 0; w < NCW; ++w) Mw = fmaxf(Mw, redM[par * NCW + w]);
@@ -245,6 +249,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 bc->lseL = static_cast<float>(lse * 1.4426950408889634);
                 bc->negk = static_cast<float>(-tr.k);
                 bc->tok = tok_ok ? tok : -1;
+                if (kChecked) bc_tag[par] = t;
                 mbar_arrive(bar_bc + 8 * par);
                 if (kPhaseCounters && p.dbg) pc.lap(d_post);  // partials in -> k published (after the peer wait)
                 if (rank == 0) {
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
 
         // copy-in + max + exp sweep + CTA reduction of row t into r[]; returns C_t.
-        auto stream_row = [&](uint32_t row_iter, bool park_prev) -> float {
+        auto stream_row = [&](int64_t t_row, uint32_t row_iter, bool park_prev) -> float {
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
                 if (park_prev) {  // park the previous row's e in TMEM, chunk by chunk
@@ -381,6 +386,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             if (lane == 0) {
                 redM[par * NCW + warp] = Mw;
                 redS[par * NCW + warp] = sw;
+                if (kChecked) red_tag[par * NCW + warp] = t_row;
                 mbar_arrive(bar_red + 8 * par);  // release: the scalar warp's wait sees the words above
             }
             if (dbg) pcc.lap(dph[1]);
@@ -393,6 +399,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             if (dbg) pcc.lap(dph[4]);
             cons_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
             if (dbg) pcc.lap(dph[3]);
+            if (kChecked) rf_check(bc_tag[par] == t);
             const Bcast* bc = bcs + par;
             const float lseL = bc->lseL;
             const float negk = bc->negk;
@@ -416,6 +423,11 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                         if (c * VPC + h < NVT) tmem_ld4(tm + 4 * (c * VPC + h), e[h]);
                 }
                 uint8_t* dc = dthr + static_cast<size_t>(c) * CHUNK_VECS * EPV * OES;
+                if (kChecked)  // every vector this chunk may store lies inside this CTA's slice of the row
+                    for (int h = 0; h < VPC; ++h)
+                        if (c * VPC + h < jmax)
+                            rf_check(c * CHUNK_VECS + h * NCT + tid < slice_len &&
+                                     slice_begin + c * CHUNK_VECS + h * NCT + tid < p.row_vecs);
                 if (c * VPC + VPC <= jfull) {  // straight-line stores (+6% over per-vector branches)
 #pragma unroll
                     for (int h = 0; h < VPC; ++h)
@@ -449,7 +461,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         uint32_t it = 0;
         int64_t t = cid;
         float C = 0.f;
-        if (t < p.T) C = stream_row(0, false);
+        if (t < p.T) C = stream_row(t, 0, false);
         while (t < p.T) {
             // park e_t in TMEM, stream row t + ncl (if any), then write row t from TMEM
             const int64_t tn = t + ncl;
@@ -459,7 +471,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             }
             if (dbg) pcc.lap(dph[2]);
             float Cn = 0.f;
-            if (tn < p.T) Cn = stream_row(it + 1, true);
+            if (tn < p.T) Cn = stream_row(tn, it + 1, true);
             tmem_wait_st();  // e_t must be in TMEM before write_row reads it back
             write_row(t, it, C);
             C = Cn;

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStatsMinBlocks) stream_stats_
     constexpr int kWarps = kStreamThreads / 32;
     __shared__ float sC[2][kWarps];
     __shared__ double sS[2][kWarps];
+    __shared__ int64_t sTag[2][kWarps];  // checked build: row of each slot
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int row_vecs = p.row_vecs;
     const int tail_vec = row_vecs - 1;
@@ -231,9 +232,12 @@ __global__ void __launch_bounds__(kStreamThreads, kStatsMinBlocks) stream_stats_
         if (lane == 0) {
             sC[par][warp] = Cw;
             sS[par][warp] = s;
+            if (kChecked) sTag[par][warp] = t;
         }
         __syncthreads();  // double-buffered slots: one barrier per row
         if (tid == 0) {
+            if (kChecked)
+                for (int w = 0; w < kWarps; ++w) rf_check(sTag[par][w] == t);
             float Cm = -CUDART_INF_F;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) Cm = fmaxf(Cm, sC[par][w]);

@@ -8,10 +8,11 @@ rows = list(csv.reader(open(sys.argv[1])))
 start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[start]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+mi = hdr.index("Metric Name")
 scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 tot, cnt = defaultdict(float), defaultdict(int)
 for r in rows[start + 1:]:
-    if len(r) <= vi:
+    if len(r) <= vi or r[mi] != "gpu__time_duration.sum":  # captures may carry dram byte metrics too
         continue
     us = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     name = r[ki].split("(")[0]

@@ -102,10 +102,10 @@ def test_rows_segment_sum_is_the_in_order_fp64_sum(dtype):
     offs[1:] = np.cumsum([len(s) for s in segs])
     idx = np.concatenate(segs).astype(np.int32)
     out = torch.full((len(segs), 1024), 3.0, dtype=torch.float64, device="cuda")
+    d_offs, d_idx = torch.from_numpy(offs).cuda(), torch.from_numpy(idx).cuda()  # alive across the launch
     st = _abi.load_library().rf_rows_segment_sum(
         rows.data_ptr(), _abi.RF_DTYPE_BF16 if dtype == torch.bfloat16 else _abi.RF_DTYPE_F32, stride,
-        torch.from_numpy(offs).cuda().data_ptr(), torch.from_numpy(idx).cuda().data_ptr(), len(segs), W,
-        out.data_ptr(), 1024, torch.cuda.current_stream().cuda_stream)
+        d_offs.data_ptr(), d_idx.data_ptr(), len(segs), W, out.data_ptr(), 1024, torch.cuda.current_stream().cuda_stream)
     assert st == 0
     host = rows.float().double().cpu().numpy()
     got = out.cpu().numpy()
