@@ -242,26 +242,26 @@ int32_t rf_debug_counters(uint64_t* out, int32_t n, int32_t reset);
  * LM-head GEMM on the tensor cores (tcgen05) with the softmax statistics fused into
  * its epilogue: for hidden states H [T, K] and the vocab projection W [V, K] (both
  * bf16, row-major, K a multiple of 64, rows 16-byte aligned), writes
- * lse[t] = log Σ_v exp((H Wᵀ)[t, v]) and x_tok[t] = (H Wᵀ)[t, token_ids[t]] (fp32)
+ * lse[t] = log Σ_v exp((H Wᵀ)[t, v]) (fp64) and x_tok[t] = (H Wᵀ)[t, token_ids[t]] (fp32)
  * without materialising the [T, V] logits.  Device pointers, stream-ordered.
  * No reference counterpart: the reference's policy is a logits table
  * (policy.hpp ToyPolicy::logits); this is the fusion §8(f) names next. */
 rf_status rf_lmhead_lse(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
-                        int32_t vocab, int32_t hidden_dim, float* lse, float* x_tok, void* stream);
+                        int32_t vocab, int32_t hidden_dim, double* lse, float* x_tok, void* stream);
 
 /* The dlogits half: recomputes the logits tiles on the tensor cores and writes
  * dlogits[t, v] = coef[t]·(1[v = token_ids[t]] − exp((H Wᵀ)[t, v] − lse[t])) as bf16 rows
  * of stride dlogits_row_stride (16-byte aligned rows), lse from rf_lmhead_lse and coef
  * the per-token loss coefficient (rf_outputs.token_coef of the loss math). */
 rf_status rf_lmhead_dlogits(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
-                            int32_t vocab, int32_t hidden_dim, const float* lse, const double* coef, void* dlogits,
+                            int32_t vocab, int32_t hidden_dim, const double* lse, const double* coef, void* dlogits,
                             int64_t dlogits_row_stride, void* stream);
 
 /* The per-token loss math between the two LM-head sweeps: lp = x_tok − lse, then the
  * surrogate, coefficient, clip flags and scalars of rf_loss_and_grad (token_mean
  * aggregation, no exact KL; batch->logits is not read).  outputs->token_coef feeds
  * rf_lmhead_dlogits; outputs->scalars accumulates like rf_loss_and_grad. */
-rf_status rf_token_loss_from_stats(const rf_loss_config* cfg, const rf_batch* batch, const float* lse,
+rf_status rf_token_loss_from_stats(const rf_loss_config* cfg, const rf_batch* batch, const double* lse,
                                    const float* x_tok, rf_outputs* outputs, void* stream);
 
 /* ---- host API: the reference-facing call with HOST buffers ----

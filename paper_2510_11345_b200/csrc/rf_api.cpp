@@ -508,7 +508,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
 }
 
 rf_status rf_lmhead_lse(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
-                        int32_t vocab, int32_t hidden_dim, float* lse, float* x_tok, void* stream) {
+                        int32_t vocab, int32_t hidden_dim, double* lse, float* x_tok, void* stream) {
     if (!hidden || !w_vocab || !token_ids || !lse || !x_tok) return RF_ERR_INVALID_ARGUMENT;
     if (num_tokens <= 0) return RF_ERR_EMPTY_BATCH;
     if (vocab < 2 || hidden_dim <= 0 || hidden_dim % 64 != 0) return RF_ERR_INVALID_ARGUMENT;
@@ -521,7 +521,7 @@ rf_status rf_lmhead_lse(const void* hidden, const void* w_vocab, const int32_t* 
 }
 
 rf_status rf_lmhead_dlogits(const void* hidden, const void* w_vocab, const int32_t* token_ids, int64_t num_tokens,
-                            int32_t vocab, int32_t hidden_dim, const float* lse, const double* coef, void* dlogits,
+                            int32_t vocab, int32_t hidden_dim, const double* lse, const double* coef, void* dlogits,
                             int64_t dlogits_row_stride, void* stream) {
     if (!hidden || !w_vocab || !token_ids || !lse || !coef || !dlogits) return RF_ERR_INVALID_ARGUMENT;
     if (num_tokens <= 0) return RF_ERR_EMPTY_BATCH;
@@ -537,7 +537,7 @@ rf_status rf_lmhead_dlogits(const void* hidden, const void* w_vocab, const int32
     return RF_OK;
 }
 
-rf_status rf_token_loss_from_stats(const rf_loss_config* c, const rf_batch* b, const float* lse, const float* x_tok,
+rf_status rf_token_loss_from_stats(const rf_loss_config* c, const rf_batch* b, const double* lse, const float* x_tok,
                                    rf_outputs* o, void* stream) {
     g_last_launches = 0;
     if (!c || !b || !o || !lse || !x_tok) return RF_ERR_INVALID_ARGUMENT;

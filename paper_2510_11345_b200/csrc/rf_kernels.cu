@@ -365,7 +365,7 @@ __global__ void seq_kernel(const __grid_constant__ KParams p, int64_t seq_begin,
 // in a fixed tree order.
 // ===========================================================================
 __global__ void __launch_bounds__(256) token_loss_kernel(const __grid_constant__ KParams p,
-                                                         const float* __restrict__ lse,
+                                                         const double* __restrict__ lse,
                                                          const float* __restrict__ xtok) {
     __shared__ double sh[RF_NUM_SCALARS][256];
     Partials part;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256) token_loss_kernel(const __grid_constant__
             tr.loss = 0.0;
             tr.flags = RF_FLAG_NONFINITE | RF_FLAG_ZERO_COEF;
         } else {
-            lp = static_cast<double>(xtok[t]) - static_cast<double>(lse[t]);
+            lp = static_cast<double>(xtok[t]) - lse[t];
             tr = token_math(p, t, lp, p.seq_of_token[t]);
             if (tr.flags & RF_FLAG_NONFINITE) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
         }
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(256) token_loss_kernel(const __grid_constant__
         for (int j = 0; j < RF_NUM_SCALARS; ++j) p.partials[static_cast<size_t>(blockIdx.x) * RF_NUM_SCALARS + j] = sh[j][0];
 }
 
-cudaError_t launch_token_loss(const KParams& p, const float* lse, const float* xtok, cudaStream_t st) {
+cudaError_t launch_token_loss(const KParams& p, const double* lse, const float* xtok, cudaStream_t st) {
     const int grid = static_cast<int>((p.T + 255) / 256);
     token_loss_kernel<<<grid, 256, 0, st>>>(p, lse, xtok);
     return cudaGetLastError();

@@ -40,9 +40,9 @@ cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int
 cudaError_t ring_kl_max_clusters(bool out_bf16, int nvt, int cs, size_t smem, int* out);
 // Experimental LM-head GEMM + fused softmax statistics (rf_lmhead.cu)
 cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
-                              float* lse, float* xtok, cudaStream_t st);
+                              double* lse, float* xtok, cudaStream_t st);
 cudaError_t launch_lmhead_dlogits(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
-                                  const float* lse, const double* coef, void* dlogits, int64_t dl_stride,
+                                  const double* lse, const double* coef, void* dlogits, int64_t dl_stride,
                                   cudaStream_t st);
 cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, int nclusters,
                             size_t smem, cudaStream_t st);
@@ -56,7 +56,7 @@ cudaError_t launch_stream_write(const KParams& p, bool in_bf16, bool out_bf16, c
 // K2st (rf_stream.cu): stats pass of sequence_product (lse, lp per token), read-only online softmax
 cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st);
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st);
-cudaError_t launch_token_loss(const KParams& p, const float* lse, const float* xtok, cudaStream_t st);
+cudaError_t launch_token_loss(const KParams& p, const double* lse, const float* xtok, cudaStream_t st);
 // K3: scalar reduce + the empty-trajectory check over the sequences this call spans
 cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, const int32_t* seq_of_token,
                             const int64_t* seq_offsets, int64_t num_tokens, int64_t num_seqs, int32_t* status,

@@ -87,7 +87,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 // dlogits of one 32-column chunk of a token row: k·(1[v = tok] − exp(x − lse)), bf16
 __device__ __forceinline__ void dl_store_chunk(__nv_bfloat16* drow, const float* v, int col0, int V, int tk, float negk,
-                                               double kd, float lseL, float lse, bool st256) {
+                                               double kd, float lseL, double lse, bool st256) {
     constexpr float L = 1.4426950408889634f;
     uint32_t w[16];
 #pragma unroll
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(192, 1)
     lmhead_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
                   const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
                   float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok,
-                  const float* __restrict__ lse_in, const double* __restrict__ coef, __nv_bfloat16* __restrict__ dl,
+                  const double* __restrict__ lse_in, const double* __restrict__ coef, __nv_bfloat16* __restrict__ dl,
                   int64_t dl_stride, int32_t nsplit, int32_t group) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(192, 1)
         const float L = 1.4426950408889634f;
         float m = -CUDART_INF_F, ssum = 0.0f, xt = 0.0f;
         // MODE 1: per-row constants
-        const float lseL = (MODE == 1 && row < T) ? lse_in[row] * L : 0.0f;
+        const float lseL = (MODE == 1 && row < T) ? static_cast<float>(lse_in[row] * 1.4426950408889634) : 0.0f;
         const double kd = (MODE == 1 && row < T) ? coef[row] : 0.0;
         const float negk = static_cast<float>(-kd);
         __nv_bfloat16* drow = (MODE == 1 && row < T) ? dl + row * dl_stride : nullptr;
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(192, 1)
     lmhead2_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
                    const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
                    float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok, int32_t nsplit,
-                   int32_t group, const float* __restrict__ lse_in, const double* __restrict__ coef,
+                   int32_t group, const double* __restrict__ lse_in, const double* __restrict__ coef,
                    __nv_bfloat16* __restrict__ dl, int64_t dl_stride) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(192, 1)
         const float L = 1.4426950408889634f;
         float m = -CUDART_INF_F, ssum = 0.0f, xt = 0.0f;
         const uint32_t acc_empty_leader = mapa(acc_empty, 0);
-        const float lseL = (MODE == 1 && row < T) ? lse_in[row] * L : 0.0f;
+        const float lseL = (MODE == 1 && row < T) ? static_cast<float>(lse_in[row] * 1.4426950408889634) : 0.0f;
         const double kd = (MODE == 1 && row < T) ? coef[row] : 0.0;
         const float negk = static_cast<float>(-kd);
         __nv_bfloat16* drow = (MODE == 1 && row < T) ? dl + row * dl_stride : nullptr;
@@ -507,7 +507,7 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
 
 // lse[t] = M + ln Σ_s ps[s][t]·exp(pm[s][t] - M), M = max_s pm[s][t] (fixed split order)
 __global__ void lmhead_combine_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int32_t nsplit,
-                                      int64_t T, float* __restrict__ lse) {
+                                      int64_t T, double* __restrict__ lse) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= T) return;
     float M = -CUDART_INF_F;
@@ -517,11 +517,11 @@ __global__ void lmhead_combine_kernel(const float* __restrict__ pm, const float*
         const float m = pm[s * T + t];
         if (m != -CUDART_INF_F) S += static_cast<double>(ps[s * T + t]) * exp(static_cast<double>(m - M));
     }
-    lse[t] = static_cast<float>(static_cast<double>(M) + log(S));
+    lse[t] = static_cast<double>(M) + log(S);  // fp64: lp = x_tok - lse keeps the 1e-5 relative budget
 }
 
 cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
-                              float* lse, float* xtok, cudaStream_t st) {
+                              double* lse, float* xtok, cudaStream_t st) {
     if (K % kLmK != 0 || T <= 0 || V <= 0) return cudaErrorInvalidValue;
     CUtensorMap mh, mw;
     if (!make_map(&mh, H, static_cast<uint64_t>(T), static_cast<uint64_t>(K), kLmM)) return cudaErrorInvalidValue;
@@ -565,7 +565,7 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
         cfg.numAttrs = 1;
         e = cudaLaunchKernelEx(&cfg, lmhead2_kernel<0>, mh, mw2, tok, T, V, K, tps, part,
                                part + static_cast<size_t>(nsplit) * T, xtok, nsplit, group2,
-                               static_cast<const float*>(nullptr), static_cast<const double*>(nullptr),
+                               static_cast<const double*>(nullptr), static_cast<const double*>(nullptr),
                                static_cast<__nv_bfloat16*>(nullptr), static_cast<int64_t>(0));
     } else {
     lmhead_kernel<0><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
@@ -580,7 +580,7 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
 }
 
 cudaError_t launch_lmhead_dlogits(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
-                                  const float* lse, const double* coef, void* dlogits, int64_t dl_stride,
+                                  const double* lse, const double* coef, void* dlogits, int64_t dl_stride,
                                   cudaStream_t st) {
     if (K % kLmK != 0 || T <= 0 || V <= 0 || (dl_stride * 2) % 16 != 0) return cudaErrorInvalidValue;
     CUtensorMap mh, mw;

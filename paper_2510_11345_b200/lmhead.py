@@ -23,7 +23,7 @@ def lmhead_lse(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch.Ten
     T, K = hidden.shape
     V = w_vocab.shape[0]
     tok = token_ids.to(device=hidden.device, dtype=torch.int32).contiguous()
-    lse = torch.empty(T, dtype=torch.float32, device=hidden.device)
+    lse = torch.empty(T, dtype=torch.float64, device=hidden.device)
     xt = torch.empty(T, dtype=torch.float32, device=hidden.device)
     lib = _abi.load_library()
     s = torch.cuda.current_stream().cuda_stream if stream is None else (
@@ -46,12 +46,12 @@ def lmhead_dlogits(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch
     padV = (V + 7) // 8 * 8
     out = torch.empty(T, padV, dtype=torch.bfloat16, device=hidden.device)
     tok = token_ids.to(device=hidden.device, dtype=torch.int32).contiguous()
-    lse32 = lse.to(torch.float32).contiguous()
+    lse64 = lse.to(torch.float64).contiguous()
     c64 = coef.to(torch.float64).contiguous()
     lib = _abi.load_library()
     s = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
-    st = lib.rf_lmhead_dlogits(hidden.data_ptr(), w_vocab.data_ptr(), tok.data_ptr(), T, V, K, lse32.data_ptr(),
+    st = lib.rf_lmhead_dlogits(hidden.data_ptr(), w_vocab.data_ptr(), tok.data_ptr(), T, V, K, lse64.data_ptr(),
                                c64.data_ptr(), out.data_ptr(), padV, s)
     if st != 0:
         from .losses import status_string
