@@ -5,20 +5,22 @@
 //   logits = H · Wᵀ      H [T, K] bf16 (hidden states), W [V, K] bf16 (vocab projection)
 //   out:   lse[t] = log Σ_v exp(logits[t, v]),  x_tok[t] = logits[t, tok_t]
 //
-// One CTA owns 128 token rows (UMMA M = 128) and sweeps the whole vocabulary in
-// 256-column tiles (UMMA N = 256), K in 64-element (128-byte, SWIZZLE_128B) chunks:
-//   warp 0      TMA producer: H and W tiles into a 4-stage shared-memory ring
-//   warp 1      one elected lane issues tcgen05.mma (kind::f16, fp32 accumulate in
-//               tensor memory), double-buffered over two 256-column TMEM accumulators
-//   warps 2-5   epilogue: tcgen05.ld of a finished tile (thread = token row), online
-//               max / Σexp in fp32 and the sampled token's logit, then release the buffer
-// The dlogits pass (a second GEMM sweep producing k·(onehot − p) tiles fed to the
-// backward GEMMs) is the next step; this kernel is the stats half, measured in TFLOP/s.
+// A 2-CTA cluster owns 256 token rows (UMMA M = 256, cta_group::2) and sweeps its
+// vocabulary split in 256-column tiles (UMMA N = 256), K in 64-element (128-byte,
+// SWIZZLE_128B) chunks:
+//   warp 0      TMA producer: each CTA's 128 H rows and half of the W tile into a
+//               6-stage shared-memory ring (bytes complete on the leader's barrier)
+//   warp 1      the leader's elected lane issues tcgen05.mma (kind::f16, fp32
+//               accumulate in tensor memory), double-buffered over two 256-column
+//               TMEM accumulators; commits multicast to both CTAs
+//   warps 2-5   epilogue: tcgen05.ld of a finished tile (thread = token row), then
+//               MODE 0 (stats): online max / Σexp in fp32 and the sampled token's logit;
+//               MODE 1 (dlogits): k·(1[v = tok] − exp(x − lse)) as bf16 rows.
+// lse is combined across the vocabulary splits in fp64 (lmhead_combine_kernel).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstdint>
 #include <math_constants.h>
 
@@ -29,19 +31,7 @@ namespace rf {
 
 namespace {
 
-constexpr int kLmM = 128, kLmN = 256, kLmK = 64, kLmStages = 4;
-constexpr uint32_t kLmAStage = kLmM * kLmK * 2;  // 16 KB
-constexpr uint32_t kLmBStage = kLmN * kLmK * 2;  // 32 KB
-constexpr uint32_t kLmStageBytes = kLmAStage + kLmBStage;
-constexpr size_t kLmSmem = static_cast<size_t>(kLmStages) * kLmStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-            "r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
-        : "memory");
-}
+constexpr int kLmM = 128, kLmN = 256, kLmK = 64;  // per CTA: 128 token rows, 256-column vocab tiles, K chunks
 
 // K-major operand tile in SWIZZLE_128B layout: rows of 128 bytes, 8-row (1024 B) groups.
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
@@ -54,21 +44,6 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
     return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, both K-major, M = 128, N = 256
-constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kLmN >> 3) << 17) |
-                              (static_cast<uint32_t>(kLmM >> 4) << 24);
-
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     uint32_t r[32];
     asm volatile(
@@ -120,6 +95,7 @@ __device__ __forceinline__ void dl_store_chunk(__nv_bfloat16* drow, const float*
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
 // Grouped raster over (128-token block, vocab split): panels of `group` token blocks; inside a
 // panel the token blocks vary fastest, so the CTAs resident together share W tiles (streamed in
 // step) and the panel's H blocks (group·128·K·2 bytes) stay L2-resident.  Split x covers vocab
@@ -129,157 +105,8 @@ __device__ __forceinline__ void dl_store_chunk(__nv_bfloat16* drow, const float*
 // MODE 0 (stats): partial (max, Σexp) per split + the sampled logit.
 // MODE 1 (dlogits): recompute the logits tile and write dlogit = k·(1[v = tok] − exp(x − lse))
 //         as bf16 rows of stride dl_stride (the input of the backward GEMMs); lse/coef per token.
-template <int MODE>
-__global__ void __launch_bounds__(192, 1)
-    lmhead_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
-                  const int32_t* __restrict__ tok, int64_t T, int32_t V, int32_t K, int32_t tps,
-                  float* __restrict__ pm, float* __restrict__ ps, float* __restrict__ xtok,
-                  const double* __restrict__ lse_in, const double* __restrict__ coef, __nv_bfloat16* __restrict__ dl,
-                  int64_t dl_stride, int32_t nsplit, int32_t group) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B tiles need 1024-byte alignment
-    const uint32_t bars = sbase + kLmStages * kLmStageBytes;
-    const uint32_t full = bars, empty = bars + 8 * kLmStages;
-    const uint32_t acc_full = bars + 16 * kLmStages, acc_empty = acc_full + 16;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (acc_empty + 16 - raw));
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nblk = (T + kLmM - 1) / kLmM;
-    const int64_t per_panel = static_cast<int64_t>(group) * nsplit;
-    const int64_t panel = blockIdx.x / per_panel, in_panel = blockIdx.x % per_panel;
-    const int64_t g0 = panel * group, gsz = (nblk - g0 < group) ? (nblk - g0) : static_cast<int64_t>(group);
-    const int64_t blk = g0 + in_panel % gsz;
-    const int split = static_cast<int>(in_panel / gsz);
-    const int64_t row0 = blk * kLmM;
-    const int ntiles_all = (V + kLmN - 1) / kLmN, nk = K / kLmK;
-    const int nbeg = split * tps;
-    const int ntiles = max(0, min(ntiles_all, nbeg + tps) - nbeg);  // tiles of this split
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kLmStages; ++s) {
-            mbar_init(full + 8 * s, 1);
-            mbar_init(empty + 8 * s, 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(acc_full + 8 * b, 1);
-            mbar_init(acc_empty + 8 * b, 4);  // the four epilogue warps
-        }
-        fence_mbar_init();
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(512)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        // ------------------------------ TMA producer ------------------------------
-        if (lane == 0) {
-            uint32_t it = 0;
-            for (int n = 0; n < ntiles; ++n) {
-                for (int kc = 0; kc < nk; ++kc, ++it) {
-                    const uint32_t s = it % kLmStages;
-                    if (it >= static_cast<uint32_t>(kLmStages)) mbar_wait(empty + 8 * s, ((it / kLmStages) - 1) & 1);
-                    const uint32_t a = sbase + s * kLmStageBytes, b = a + kLmAStage;
-                    mbar_arrive_expect_tx(full + 8 * s, kLmStageBytes);
-                    tma_load_2d(a, &tmH, kc * kLmK, static_cast<int>(row0), full + 8 * s);
-                    tma_load_2d(b, &tmW, kc * kLmK, (nbeg + n) * kLmN, full + 8 * s);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------- MMA issuer -------------------------------
-        if (lane == 0) {
-            uint32_t it = 0;
-            for (int n = 0; n < ntiles; ++n) {
-                const uint32_t buf = n & 1;
-                if (n >= 2) mbar_wait(acc_empty + 8 * buf, ((n >> 1) - 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t d = tmem + buf * kLmN;
-                for (int kc = 0; kc < nk; ++kc, ++it) {
-                    const uint32_t s = it % kLmStages;
-                    mbar_wait(full + 8 * s, (it / kLmStages) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t a = sbase + s * kLmStageBytes, b = a + kLmAStage;
-#pragma unroll
-                    for (int k = 0; k < kLmK / 16; ++k)  // UMMA K = 16: +32 bytes inside the 128-byte swizzle atom
-                        umma_f16(d, smem_desc_sw128(a + 32 * k), smem_desc_sw128(b + 32 * k), kLmIdesc,
-                                 (kc > 0 || k > 0) ? 1u : 0u);
-                    umma_commit(empty + 8 * s);  // frees the stage when these MMAs have read it
-                }
-                umma_commit(acc_full + 8 * buf);  // the tile's accumulator is complete
-            }
-        }
-    } else {
-        // -------------------------------- epilogue --------------------------------
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int64_t row = row0 + 32 * q + lane;
-        const int32_t tk = row < T ? tok[row] : -1;
-        const float L = 1.4426950408889634f;
-        float m = -CUDART_INF_F, ssum = 0.0f, xt = 0.0f;
-        // MODE 1: per-row constants
-        const float lseL = (MODE == 1 && row < T) ? static_cast<float>(lse_in[row] * 1.4426950408889634) : 0.0f;
-        const double kd = (MODE == 1 && row < T) ? coef[row] : 0.0;
-        const float negk = static_cast<float>(-kd);
-        __nv_bfloat16* drow = (MODE == 1 && row < T) ? dl + row * dl_stride : nullptr;
-        const bool st256 = MODE == 1 && (dl_stride * 2) % 32 == 0 && (reinterpret_cast<uintptr_t>(dl) & 31) == 0;
-        for (int n = 0; n < ntiles; ++n) {
-            const uint32_t buf = n & 1;
-            mbar_wait_sleep(acc_full + 8 * buf, (n >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kLmN;
-#pragma unroll 1
-            for (int c = 0; c < kLmN; c += 32) {
-                float v[32];
-                tmem_ld32(taddr + c, v);
-                const int col0 = (nbeg + n) * kLmN + c;
-                if constexpr (MODE == 1) {
-                    if (drow == nullptr) continue;
-                    dl_store_chunk(drow, v, col0, V, tk, negk, kd, lseL, lse_in[row], st256);
-                    continue;
-                }
-                float cm = -CUDART_INF_F;
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (col0 + i < V) cm = fmaxf(cm, v[i]);
-                const float mn = fmaxf(m, cm);
-                float acc = 0.0f;
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (col0 + i < V) acc += ex2_approx((v[i] - mn) * L);
-                ssum = (m == -CUDART_INF_F ? 0.0f : ssum * ex2_approx((m - mn) * L)) + acc;
-                m = mn;
-                if (tk >= col0 && tk < col0 + 32) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (tk == col0 + i) xt = v[i];
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
-        }
-        if (MODE == 0 && row < T) {
-            pm[static_cast<int64_t>(split) * T + row] = m;
-            ps[static_cast<int64_t>(split) * T + row] = ssum;
-            if (tk >= nbeg * kLmN && tk < (nbeg + ntiles) * kLmN) xtok[row] = xt;
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
-}
-
 // ---------------------------------------------------------------------------
-// 2-CTA stats sweep (default; RF_LMHEAD_2CTA=0 selects lmhead_kernel<0>): a cluster pair computes a
+// 2-CTA sweep: a cluster pair computes a
 // 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256, N = 256); each CTA stages its
 // own 128 H rows and half (128 rows) of the W tile, so operand traffic per FLOP halves.
 // The leader (rank 0) issues the MMAs; its full barriers collect both CTAs' TMA bytes;
@@ -520,61 +347,67 @@ __global__ void lmhead_combine_kernel(const float* __restrict__ pm, const float*
     lse[t] = static_cast<double>(M) + log(S);  // fp64: lp = x_tok - lse keeps the 1e-5 relative budget
 }
 
-cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
-                              double* lse, float* xtok, cudaStream_t st) {
+namespace {
+
+// One 2-CTA sweep over the vocabulary: token pairs of 256 rows x vocab splits, split so
+// that pairs x splits fill the SMs for ~8 waves; grouped raster for L2 reuse of W.
+template <int MODE>
+cudaError_t launch_lmhead2(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
+                           float* pm, float* ps, float* xtok, const double* lse, const double* coef,
+                           __nv_bfloat16* dl, int64_t dl_stride, int* nsplit_out, cudaStream_t st) {
     if (K % kLmK != 0 || T <= 0 || V <= 0) return cudaErrorInvalidValue;
     CUtensorMap mh, mw;
     if (!make_map(&mh, H, static_cast<uint64_t>(T), static_cast<uint64_t>(K), kLmM)) return cudaErrorInvalidValue;
-    if (!make_map(&mw, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), kLmN)) return cudaErrorInvalidValue;
-    cudaError_t e =
-        cudaFuncSetAttribute(lmhead_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kLmSmem));
-    if (e != cudaSuccess) return e;
+    if (!make_map(&mw, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), 128)) return cudaErrorInvalidValue;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // split the vocabulary so that token blocks x splits fill the SMs for ~8 waves
     const int64_t nblk = (T + kLmM - 1) / kLmM;
     const int ntiles = (V + kLmN - 1) / kLmN;
     int nsplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, (8LL * sms + nblk - 1) / nblk)));
     const int tps = (ntiles + nsplit - 1) / nsplit;
     nsplit = (ntiles + tps - 1) / tps;
+    if (nsplit_out) *nsplit_out = nsplit;
+    if (MODE == 0 && !pm) return cudaSuccess;  // sizing query
+    cudaError_t e = cudaFuncSetAttribute(lmhead2_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kL2Smem));
+    if (e != cudaSuccess) return e;
+    const int64_t npair = (T + 255) / 256;
+    const int group2 = std::max(1, lm_group(npair, K) / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * npair * nsplit));
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = kL2Smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, lmhead2_kernel<MODE>, mh, mw, tok, T, V, K, tps, pm, ps, xtok, nsplit, group2,
+                              lse, coef, dl, dl_stride);
+}
+
+}  // namespace
+
+cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
+                              double* lse, float* xtok, cudaStream_t st) {
+    int nsplit = 0;
+    cudaError_t e = launch_lmhead2<0>(H, W, tok, T, V, K, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                      &nsplit, st);
+    if (e != cudaSuccess) return e;
     float* part = nullptr;
     e = cudaMallocAsync(&part, static_cast<size_t>(2) * nsplit * T * sizeof(float), st);
     if (e != cudaSuccess) return e;
-    const int group = lm_group(nblk, K);
-    const char* two = std::getenv("RF_LMHEAD_2CTA");  // default on; "0" selects the one-CTA kernel
-    if (!(two && two[0] == '0')) {
-        CUtensorMap mw2;
-        if (!make_map(&mw2, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), 128)) return cudaErrorInvalidValue;
-        e = cudaFuncSetAttribute(lmhead2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kL2Smem));
-        if (e != cudaSuccess) return e;
-        const int64_t npair = (T + 255) / 256;
-        const int group2 = std::max(1, lm_group(npair, K) / 2);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(2 * npair * nsplit));
-        cfg.blockDim = dim3(192);
-        cfg.dynamicSmemBytes = kL2Smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, lmhead2_kernel<0>, mh, mw2, tok, T, V, K, tps, part,
-                               part + static_cast<size_t>(nsplit) * T, xtok, nsplit, group2,
-                               static_cast<const double*>(nullptr), static_cast<const double*>(nullptr),
-                               static_cast<__nv_bfloat16*>(nullptr), static_cast<int64_t>(0));
-    } else {
-    lmhead_kernel<0><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
-        mh, mw, tok, T, V, K, tps, part, part + static_cast<size_t>(nsplit) * T, xtok, nullptr, nullptr, nullptr, 0,
-        nsplit, group);
+    e = launch_lmhead2<0>(H, W, tok, T, V, K, part, part + static_cast<size_t>(nsplit) * T, xtok, nullptr, nullptr,
+                          nullptr, 0, nullptr, st);
+    if (e == cudaSuccess) {
+        lmhead_combine_kernel<<<static_cast<unsigned>((T + 255) / 256), 256, 0, st>>>(
+            part, part + static_cast<size_t>(nsplit) * T, nsplit, T, lse);
+        e = cudaGetLastError();
     }
-    lmhead_combine_kernel<<<static_cast<unsigned>((T + 255) / 256), 256, 0, st>>>(
-        part, part + static_cast<size_t>(nsplit) * T, nsplit, T, lse);
-    e = cudaGetLastError();
     cudaFreeAsync(part, st);
     return e;
 }
@@ -582,51 +415,9 @@ cudaError_t launch_lmhead_lse(const void* H, const void* W, const int32_t* tok, 
 cudaError_t launch_lmhead_dlogits(const void* H, const void* W, const int32_t* tok, int64_t T, int32_t V, int32_t K,
                                   const double* lse, const double* coef, void* dlogits, int64_t dl_stride,
                                   cudaStream_t st) {
-    if (K % kLmK != 0 || T <= 0 || V <= 0 || (dl_stride * 2) % 16 != 0) return cudaErrorInvalidValue;
-    CUtensorMap mh, mw;
-    if (!make_map(&mh, H, static_cast<uint64_t>(T), static_cast<uint64_t>(K), kLmM)) return cudaErrorInvalidValue;
-    if (!make_map(&mw, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), kLmN)) return cudaErrorInvalidValue;
-    cudaError_t e =
-        cudaFuncSetAttribute(lmhead_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kLmSmem));
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t nblk = (T + kLmM - 1) / kLmM;
-    const int ntiles = (V + kLmN - 1) / kLmN;
-    int nsplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, (8LL * sms + nblk - 1) / nblk)));
-    const int tps = (ntiles + nsplit - 1) / nsplit;
-    nsplit = (ntiles + tps - 1) / tps;
-    const int group = lm_group(nblk, K);
-    const char* two = std::getenv("RF_LMHEAD_2CTA");  // default on; "0" selects the one-CTA kernel
-    if (!(two && two[0] == '0')) {
-        CUtensorMap mw2;
-        if (!make_map(&mw2, W, static_cast<uint64_t>(V), static_cast<uint64_t>(K), 128)) return cudaErrorInvalidValue;
-        e = cudaFuncSetAttribute(lmhead2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kL2Smem));
-        if (e != cudaSuccess) return e;
-        const int64_t npair = (T + 255) / 256;
-        const int group2 = std::max(1, lm_group(npair, K) / 2);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(2 * npair * nsplit));
-        cfg.blockDim = dim3(192);
-        cfg.dynamicSmemBytes = kL2Smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, lmhead2_kernel<1>, mh, mw2, tok, T, V, K, tps, static_cast<float*>(nullptr),
-                                  static_cast<float*>(nullptr), static_cast<float*>(nullptr), nsplit, group2, lse,
-                                  coef, static_cast<__nv_bfloat16*>(dlogits), dl_stride);
-    }
-    lmhead_kernel<1><<<static_cast<unsigned>(nblk * nsplit), 192, kLmSmem, st>>>(
-        mh, mw, tok, T, V, K, tps, nullptr, nullptr, nullptr, lse, coef, static_cast<__nv_bfloat16*>(dlogits),
-        dl_stride, nsplit, group);
-    return cudaGetLastError();
+    if ((dl_stride * 2) % 16 != 0) return cudaErrorInvalidValue;
+    return launch_lmhead2<1>(H, W, tok, T, V, K, nullptr, nullptr, nullptr, lse, coef,
+                             static_cast<__nv_bfloat16*>(dlogits), dl_stride, nullptr, st);
 }
 
 }  // namespace rf

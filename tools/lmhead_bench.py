@@ -92,6 +92,29 @@ def composed():
 
 ms_composed = timed(composed)
 ms_pipeline = timed(lambda: lmhead_loss_and_grad(cfg, H, W, pb, check=False))
+
+
+def composed_grads():  # + the backward GEMMs of the materialised dlogits (cuBLAS, fp32 out)
+    composed()
+    dl = op.dlogits
+    return torch.mm(dl, W, out_dtype=torch.float32), torch.mm(dl.t(), H, out_dtype=torch.float32)
+
+
+ms_composed_grads = timed(composed_grads)
+ms_pipeline_grads = timed(lambda: lmhead_loss_and_grad(cfg, H, W, pb, check=False, want="grads"))
+def peak_gb(fn):
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    fn()
+    torch.cuda.synchronize()
+    return round((torch.cuda.max_memory_allocated() - base) / 1e9, 2)
+
+
+peak_fused = peak_gb(lambda: lmhead_loss_and_grad(cfg, H, W, pb, check=False, want="grads"))
+peak_composed = peak_gb(composed_grads)  # logits_buf and op.dlogits are preallocated: add them below
+ms_bwd_gemms = timed(lambda: (torch.mm(op.dlogits, W, out_dtype=torch.float32),
+                              torch.mm(op.dlogits.t(), H, out_dtype=torch.float32)))
 peaks = {}
 try:
     with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as f:
@@ -107,5 +130,10 @@ out = {"tokens": T, "vocab": V, "hidden": K, "fused_ms": round(ms_fused, 3),
        "fused_stats_plus_dlogits_ms": round(ms_fused + ms_dl, 3),
        "cublas_gemm_plus_torch_softmax_dlogits_ms": None if ms_unfused_dl is None else round(ms_unfused_dl, 3),
        "loss_and_dlogits_fused_pipeline_ms": round(ms_pipeline, 3),
-       "loss_and_dlogits_cublas_logits_plus_ring_kernel_ms": round(ms_composed, 3)}
+       "loss_and_dlogits_cublas_logits_plus_ring_kernel_ms": round(ms_composed, 3),
+       "loss_and_grads_fused_pipeline_ms": round(ms_pipeline_grads, 3),
+       "loss_and_grads_composed_ms": round(ms_composed_grads, 3),
+       "backward_gemms_cublas_ms": round(ms_bwd_gemms, 3),
+       "peak_extra_GB_fused_grads": peak_fused,
+       "peak_extra_GB_composed_grads": round(peak_composed + 2 * T * V * 2 / 1e9, 2)}
 print(json.dumps(out))
