@@ -275,7 +275,7 @@ def impl_reference(args, wl, variant):
 # ---------------------------------------------------------------------------
 # Our arm
 # ---------------------------------------------------------------------------
-def e2e_host_api(cfg, dw, tokens, world, steps=3, warmup=1, chunk=512):
+def e2e_host_api(cfg, dw, tokens, world, steps=3, warmup=1, chunk=512, ref_pool=None):
     """The reference-facing C-ABI call with HOST buffers (rf_loss_and_grad_host), on
     every rank at once: pinned host logits rows in, pinned host dlogits + per-token
     outputs + scalars out; every H2D/D2H copy is inside the timed region.  Returns the
@@ -305,6 +305,11 @@ def e2e_host_api(cfg, dw, tokens, world, steps=3, warmup=1, chunk=512):
     for r0 in range(0, T, 4096):
         h_logits[r0:r0 + 4096].copy_(dw.pool[rows[r0:r0 + 4096]].cpu())
     h_dl = torch.empty(T, V, dtype=torch.bfloat16, pin_memory=True)
+    h_ref = None
+    if ref_pool is not None:  # exact KL: the reference-policy row of every token too
+        h_ref = torch.empty(T, V, dtype=torch.bfloat16, pin_memory=True)
+        for r0 in range(0, T, 4096):
+            h_ref[r0:r0 + 4096].copy_(ref_pool[rows[r0:r0 + 4096]].cpu())
 
     def pin(t):
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
@@ -331,6 +336,8 @@ def e2e_host_api(cfg, dw, tokens, world, steps=3, warmup=1, chunk=512):
     b.logp_dtype, b.normalization = _abi.RF_DTYPE_F32, _abi.RF_NORM_GLOBAL_TOKEN
     b.behavior_logp, b.prox_logp, b.engine_logp = h_b.data_ptr(), h_q.data_ptr(), h_e.data_ptr()
     b.global_num_seqs, b.global_num_tokens, b.grad_sign = n_seq, T, 1.0
+    if h_ref is not None:
+        b.ref_logits, b.ref_row_stride = h_ref.data_ptr(), V
     o = _abi.rf_outputs()
     o.dlogits, o.dlogits_dtype, o.dlogits_row_stride = h_dl.data_ptr(), _abi.RF_DTYPE_BF16, V
     o.token_logp, o.token_ratio = outs["lp"].data_ptr(), outs["ratio"].data_ptr()
@@ -358,7 +365,7 @@ def e2e_host_api(cfg, dw, tokens, world, steps=3, warmup=1, chunk=512):
     else:
         T_all = T
     t = statistics.median(tt[:-1].tolist())
-    h2d = T * V * 2 + T * (4 + 4 + 4 * 3) + (n_seq + 1) * 8 + n_seq * 8
+    h2d = T * V * 2 * (2 if h_ref is not None else 1) + T * (4 + 4 + 4 * 3) + (n_seq + 1) * 8 + n_seq * 8
     d2h = T * V * 2 + T * (8 * 4 + 1) + _abi.RF_NUM_SCALARS * 8 + 4
     return {"value": T_all / t, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d * world),
             "d2h_bytes_per_step": int(d2h * world),
@@ -576,7 +583,8 @@ def impl_ours(args, wl, variant):
     e2e = None
     if not args.no_e2e:
         try:
-            e2e = e2e_host_api(cfg, dw, args.e2e_tokens if world == 1 else min(args.e2e_tokens, 8192), world)
+            e2e = e2e_host_api(cfg, dw, args.e2e_tokens if world == 1 else min(args.e2e_tokens, 8192), world,
+                               ref_pool=ref_pool)
         except Exception as exc:  # report, do not hide
             e2e = {"value": None, "unit": "tokens/s", "error": repr(exc)}
     parity = None
