@@ -33,6 +33,10 @@ using namespace ring;
 
 namespace {
 
+#ifndef RF_KL_FOLD
+#define RF_KL_FOLD 1  // vectors per fp32 partial before the fp64 fold (A/B)
+#endif
+
 // One 8-element vector of x and of y: e (f16x2) replaces x, d = x - y (f16x2)
 // replaces y; packed f32x2 partial sums of e, ey and e·d are accumulated.
 __device__ __forceinline__ void kl_vec(uint4& vx, uint4& vy, uint64_t L2, uint64_t negC2, uint64_t negCy2,
@@ -502,14 +506,23 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
             const float C = ((M == -CUDART_INF_F) ? 0.0f : M) * kL2e;
             const float Cy = ((My == -CUDART_INF_F) ? 0.0f : My) * kL2e;
             const uint64_t negC2 = pk2(-C, -C), negCy2 = pk2(-Cy, -Cy);
+            // packed fp32 partial sums over RF_KL_FOLD vectors, folded into fp64
             double S = 0.0, T = 0.0, Sy = 0.0;
+            uint64_t as = 0, ay = 0, ad = 0;
 #pragma unroll
             for (int j = 0; j < NVT; ++j) {
                 uint64_t se, sy, sd;
                 kl_vec(r[j], ry[j], L2, negC2, negCy2, se, sy, sd);
-                S += static_cast<double>(lo2(se) + hi2(se));
-                Sy += static_cast<double>(lo2(sy) + hi2(sy));
-                T += static_cast<double>(lo2(sd) + hi2(sd));
+                if (j % RF_KL_FOLD == 0) {
+                    as = se, ay = sy, ad = sd;
+                } else {
+                    as = fadd2(as, se), ay = fadd2(ay, sy), ad = fadd2(ad, sd);
+                }
+                if (j % RF_KL_FOLD == RF_KL_FOLD - 1 || j == NVT - 1) {
+                    S += static_cast<double>(lo2(as) + hi2(as));
+                    Sy += static_cast<double>(lo2(ay) + hi2(ay));
+                    T += static_cast<double>(lo2(ad) + hi2(ad));
+                }
             }
             const float Mr = (S == 0.0) ? -CUDART_INF_F : C;
             const float Myr = (Sy == 0.0) ? -CUDART_INF_F : Cy;
