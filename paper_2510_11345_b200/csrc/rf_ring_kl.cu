@@ -33,9 +33,8 @@ using namespace ring;
 
 namespace {
 
-#ifndef RF_KL_FOLD
-#define RF_KL_FOLD 1  // vectors per fp32 partial before the fp64 fold (A/B)
-#endif
+// vectors per packed fp32 partial before the fp64 fold (measured on B200: 2 is +1.2% over 1; 4 gains nothing)
+constexpr int kKlFold = 2;
 
 // One 8-element vector of x and of y: e (f16x2) replaces x, d = x - y (f16x2)
 // replaces y; packed f32x2 partial sums of e, ey and e·d are accumulated.
@@ -506,19 +505,19 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
             const float C = ((M == -CUDART_INF_F) ? 0.0f : M) * kL2e;
             const float Cy = ((My == -CUDART_INF_F) ? 0.0f : My) * kL2e;
             const uint64_t negC2 = pk2(-C, -C), negCy2 = pk2(-Cy, -Cy);
-            // packed fp32 partial sums over RF_KL_FOLD vectors, folded into fp64
+            // packed fp32 partial sums over kKlFold vectors, folded into fp64
             double S = 0.0, T = 0.0, Sy = 0.0;
             uint64_t as = 0, ay = 0, ad = 0;
 #pragma unroll
             for (int j = 0; j < NVT; ++j) {
                 uint64_t se, sy, sd;
                 kl_vec(r[j], ry[j], L2, negC2, negCy2, se, sy, sd);
-                if (j % RF_KL_FOLD == 0) {
+                if (j % kKlFold == 0) {
                     as = se, ay = sy, ad = sd;
                 } else {
                     as = fadd2(as, se), ay = fadd2(ay, sy), ad = fadd2(ad, sd);
                 }
-                if (j % RF_KL_FOLD == RF_KL_FOLD - 1 || j == NVT - 1) {
+                if (j % kKlFold == kKlFold - 1 || j == NVT - 1) {
                     S += static_cast<double>(lo2(as) + hi2(as));
                     Sy += static_cast<double>(lo2(ay) + hi2(ay));
                     T += static_cast<double>(lo2(ad) + hi2(ad));
