@@ -501,6 +501,14 @@ def loss_and_grad_policy(config: LossConfig, policy_logits, batch: Sequence[Traj
     if ref_logits is not None and config.variant == LossVariant.grpo and config.kl_weight > 0.0:
         pb.ref_logits = table(ref_logits)
     res = loss_and_grad(config, pb, dlogits_dtype=torch.float32)
-    grad = torch.zeros(C, V, dtype=torch.float64, device=dev)
-    grad.index_add_(0, pb.row_of_token.to(torch.int64), res.dlogits.to(torch.float64))
+    # LossResult.grad: per-context fp64 sums of the per-token dlogits rows in token order
+    # (rf_rows_segment_sum, deterministic — LogProbGrad's per-context accumulation, losses.cpp:87-115)
+    order = torch.argsort(rows, stable=True)
+    seg = torch.zeros(C + 1, dtype=torch.int64)
+    seg[1:] = torch.cumsum(torch.bincount(rows.to(torch.int64), minlength=C), 0)
+    d_seg, d_idx = seg.to(dev), order.to(torch.int32).to(dev)
+    grad = torch.empty(C, V, dtype=torch.float64, device=dev)
+    _raise_for(_lib().rf_rows_segment_sum(res.dlogits.data_ptr(), _abi.RF_DTYPE_F32, int(res.dlogits.stride(0)),
+                                          d_seg.data_ptr(), d_idx.data_ptr(), C, V, grad.data_ptr(), V,
+                                          _stream_handle(None)))
     return PolicyLossResult(value=res.value, grad=grad.reshape(-1).cpu())

@@ -56,3 +56,31 @@ def test_toy_train_loop_on_gpu_matches_reference(variant, agg, lag, steps, lr, n
     assert np.abs(cpu["reward"] - gpu["reward"]).max() < 2e-3, np.abs(cpu["reward"] - gpu["reward"]).max()
     assert abs(cpu["final_reward"] - gpu["final_reward"]) < 1e-3 * cpu["final_reward"]
     assert gpu["final_reward"] > gpu["reward"][0] + 0.05 or steps < 50
+
+
+@pytest.mark.parametrize("key", [k for k in np.load(GOLDEN)["loss_cases"] if str(k).startswith("B_")])
+def test_python_policy_api_matches_reference_golden(key):
+    """The rlsim-shaped Python API (losses.loss_and_grad_policy: Trajectory list + logits
+    tables, grad folded per context on the device by rf_rows_segment_sum) on the same
+    golden cases as the C++ shim."""
+    import paper_2510_11345_b200 as rf
+
+    g = np.load(GOLDEN)
+    agg = "sequence_product" if "_sequence_product_" in key else "token_mean"
+    v = key.split("_" + agg + "_")[1]
+    kl = v == "grpo"
+    cfg = config(v, aggregation=agg, kl_weight=0.1 if kl else 0.0, engine_mismatch_cap=2.0)
+    k = lambda n: g[key + "/" + n] if (key + "/" + n) in g.files else None  # noqa: E731
+    offs, ctx, tok, beh, eng = k("seq_offsets"), k("traj_context"), k("tokens"), k("behavior"), k("engine")
+    batch = [rf.Trajectory(context=int(ctx[i]), tokens=tok[offs[i]:offs[i + 1]].tolist(),
+                           advantage=float(k("advantages")[i]), behavior_logp=beh[offs[i]:offs[i + 1]].tolist(),
+                           engine_logp=[] if eng is None else eng[offs[i]:offs[i + 1]].tolist())
+             for i in range(len(ctx))]
+    res = rf.loss_and_grad_policy(cfg, k("logits"), batch, prox_logits=k("prox_table"), ref_logits=k("ref_logits"))
+    ref_val, ref_grad = float(k("value")[0]), k("grad").reshape(-1)
+    grad = res.grad.numpy()
+    scale = np.abs(ref_grad).max()
+    assert abs(res.value - ref_val) <= 1e-5 * max(abs(ref_val), 1e-3 * np.abs(ref_grad).sum()), (res.value, ref_val)
+    assert np.abs(grad - ref_grad).max() <= 1e-4 * scale + 1e-9, np.abs(grad - ref_grad).max() / scale
+    again = rf.loss_and_grad_policy(cfg, k("logits"), batch, prox_logits=k("prox_table"), ref_logits=k("ref_logits"))
+    assert np.array_equal(again.grad.numpy(), grad)  # deterministic fold
