@@ -65,6 +65,18 @@ __device__ __forceinline__ uint4 neg_inf_vec() {
                    : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
 }
 
+// The same fill built by volatile moves: the compiler may not hoist it out of the
+// rarely taken branch it is written in (a plain constant fill was hoisted above the
+// chunk loads and executed for every chunk of every row: 4 moves per vector).
+template <bool IN_BF16>
+__device__ __forceinline__ uint4 neg_inf_vec_here() {
+    uint4 v;
+    asm volatile("mov.b32 %0, %4;\n\tmov.b32 %1, %4;\n\tmov.b32 %2, %4;\n\tmov.b32 %3, %4;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "n"(IN_BF16 ? 0xff80ff80u : 0xff800000u));
+    return v;
+}
+
 template <bool IN_BF16>
 __device__ __forceinline__ void mask_tail(uint4& v, int valid) {
     uint32_t w[4] = {v.x, v.y, v.z, v.w};

@@ -469,14 +469,25 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 }
                 if (c < nchunks) {
                     cons_wait(bar_full + 8 * s, fphase);
-                    const uint32_t slot = sbase + s * SLOT_BYTES;
+                    const uint32_t slot = sbase + s * SLOT_BYTES + tid * 16;
+                    if (c * VPC + VPC <= jmax) {  // whole chunk inside the slice: plain loads
 #pragma unroll
-                    for (int jj = 0; jj < VPC; ++jj) {
-                        const int j = c * VPC + jj;
-                        if (j < NVT) {
-                            const bool ok = j < jmax;
-                            r[j] = ok ? lds128(slot + (jj * NCT + tid) * 16) : neg_inf_vec<true>();
-                            ry[j] = ok ? lds128(slot + CHUNK_BYTES + (jj * NCT + tid) * 16) : neg_inf_vec<true>();
+                        for (int jj = 0; jj < VPC; ++jj) {
+                            const int j = c * VPC + jj;
+                            if (j < NVT) {
+                                r[j] = lds128(slot + jj * NCT * 16);
+                                ry[j] = lds128(slot + CHUNK_BYTES + jj * NCT * 16);
+                            }
+                        }
+                    } else {  // the slice ends in this chunk: -inf past it
+#pragma unroll
+                        for (int jj = 0; jj < VPC; ++jj) {
+                            const int j = c * VPC + jj;
+                            if (j < NVT) {
+                                const bool ok = j < jmax;
+                                r[j] = ok ? lds128(slot + jj * NCT * 16) : neg_inf_vec_here<true>();
+                                ry[j] = ok ? lds128(slot + CHUNK_BYTES + jj * NCT * 16) : neg_inf_vec_here<true>();
+                            }
                         }
                     }
                     __syncwarp();
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
 #pragma unroll
                     for (int jj = 0; jj < VPC; ++jj) {
                         const int j = c * VPC + jj;
-                        if (j < NVT) r[j] = ry[j] = neg_inf_vec<true>();
+                        if (j < NVT) r[j] = ry[j] = neg_inf_vec_here<true>();
                     }
                 }
             }

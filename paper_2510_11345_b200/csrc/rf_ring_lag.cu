@@ -320,12 +320,19 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     if (dbg) pcc.lap(dph[1]);
                     cons_wait(bar_full + 8 * s, fphase);
                     if (dbg) pcc.lap(dph[0]);
-                    const uint32_t slot = sbase + s * CHUNK_BYTES;
+                    const uint32_t slot = sbase + s * CHUNK_BYTES + tid * 16;
+                    if (c * VPC + VPC <= jmax) {  // whole chunk inside the slice: plain loads
 #pragma unroll
-                    for (int jj = 0; jj < VPC; ++jj) {
-                        const int j = c * VPC + jj;
-                        if (j < NVT)
-                            r[j] = (j < jmax) ? lds128(slot + (jj * NCT + tid) * 16) : neg_inf_vec<IN_BF16>();
+                        for (int jj = 0; jj < VPC; ++jj) {
+                            const int j = c * VPC + jj;
+                            if (j < NVT) r[j] = lds128(slot + jj * NCT * 16);
+                        }
+                    } else {  // the slice ends in this chunk: -inf past it
+#pragma unroll
+                        for (int jj = 0; jj < VPC; ++jj) {
+                            const int j = c * VPC + jj;
+                            if (j < NVT) r[j] = (j < jmax) ? lds128(slot + jj * NCT * 16) : neg_inf_vec_here<IN_BF16>();
+                        }
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bar_empty + 8 * s);
@@ -337,7 +344,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
 #pragma unroll
                     for (int jj = 0; jj < VPC; ++jj) {
                         const int j = c * VPC + jj;
-                        if (j < NVT) r[j] = neg_inf_vec<IN_BF16>();
+                        if (j < NVT) r[j] = neg_inf_vec_here<IN_BF16>();
                     }
                 }
             }
