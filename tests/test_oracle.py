@@ -229,3 +229,39 @@ def test_reference_train_loop_golden():
         r = O.ref_train_loop(config("tis", aggregation="sequence_product"), contexts=4, arms=10, group_size=8,
                              traj_len=4, steps=300, lr=2.0, reward_noise=0.1, async_lag=8, seed=1212)
         assert r["final_reward"] == float(g["train/offpolicy_tis/final_reward"][0])
+
+
+def test_sampled_row_checker_accepts_oracle_and_rejects_perturbations():
+    """oracle/check.py (bench.py's --check leg): the oracle's own outputs pass, and a
+    perturbed lp, a flipped flag, a coefficient taken from another row, or a dlogits row
+    off by more than 2e-3·|k| are each rejected."""
+    from oracle.check import check_sample
+    from tests.cases import make_case
+
+    case = make_case(61, T_seqs=12, G=4, V=257, max_len=5, mapping="A", stale=0.3)
+    cfg = config("decoupled_ppo", engine_mismatch_cap=2.0)
+    kw = dict(logits=case.logits, token_ids=case.token_ids, seq_offsets=case.seq_offsets,
+              advantages=case.advantages, behavior_logp=case.behavior_logp, prox_logp=case.prox_logp,
+              engine_logp=case.engine_logp, ref_logits=None, normalization=1, global_num_seqs=case.N,
+              global_num_tokens=case.T)
+    ref = O.oracle_loss_and_grad(cfg, case.logits, case.token_ids, case.seq_offsets, case.advantages,
+                                 case.behavior_logp, prox_logp=case.prox_logp, engine_logp=case.engine_logp,
+                                 normalization=1)
+    good = {"lp": ref["token_logp"].copy(), "ratio": ref["token_ratio"].copy(), "coef": ref["token_coef"].copy(),
+            "loss": ref["token_loss"].copy(), "flags": ref["token_flags"].copy()}
+    dl = {i: ref["dlogits"][i].copy() for i in range(0, case.T, 3)}
+    assert check_sample(cfg, gpu=good, dl_rows=dl, **kw)["ok"]
+
+    def bad(mut, rows=None):
+        g = {k: v.copy() for k, v in good.items()}
+        mut(g)
+        return not check_sample(cfg, gpu=g, dl_rows=dl if rows is None else rows, **kw)["ok"]
+
+    nz = int(np.nonzero(good["coef"])[0][0])
+    assert bad(lambda g: g["lp"].__setitem__(0, g["lp"][0] * (1 + 1e-4)))
+    assert bad(lambda g: g["flags"].__setitem__(1, g["flags"][1] ^ 0x01))
+    assert bad(lambda g: g["coef"].__setitem__(nz, g["coef"][(nz + 1) % case.T] + 1e-9))
+    rows = dict(dl)
+    r0 = next(iter(rows))
+    rows[r0] = rows[r0] + 3e-3 * max(abs(good["coef"][r0]), 1e-12)
+    assert bad(lambda g: None, rows) or good["coef"][r0] == 0
