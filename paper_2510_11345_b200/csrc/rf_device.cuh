@@ -287,6 +287,14 @@ __device__ __forceinline__ void st_relaxed_gpu_f32(float* a, float v) {
 __device__ __forceinline__ void st_release_gpu_u64(unsigned long long* a, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* a) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");

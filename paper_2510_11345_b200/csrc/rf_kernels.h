@@ -32,7 +32,9 @@ constexpr size_t kRingLagBarrierBytes = 48;
 
 // Exact-KL lag kernel (rf_ring_kl.cu): policy and reference rows co-resident,
 // 12 consumer warps, bf16 logits; NVT = 13 covers a quarter Qwen3 row (4-CTA cluster).
-constexpr int kRingNvtKL[3] = {4, 10, 13};  // 13: 4-CTA groups at V=151,936 (5-CTA groups at NVT 10 measured -6%)
+// 13: 4-CTA groups at V = 151,936 (larger groups lose: 5-CTA groups at NVT 10 -12%, 7-CTA at NVT 8 -40%,
+// profiles/r02_ab/kl_group_and_exchange_ab.txt)
+constexpr int kRingNvtKL[3] = {4, 10, 13};
 // [4][8] 40-byte exchange slots + 5 x [2][NCW] partials + broadcast (+ checked-build row tags)
 constexpr size_t kRingKLTailBytes = RF_CHECKED ? 2176 + 2 * 16 * 8 + 16 : 2176;
 cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int nclusters, size_t smem,

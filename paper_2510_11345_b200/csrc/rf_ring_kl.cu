@@ -258,6 +258,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
             Partials part;
             part.zero();
             uint32_t row_iter = which;
+            unsigned long long d_red = 0, d_x = 0, d_math = 0;  // phase counters (profiling build)
+            PhaseClock pc;
+            pc.start();
+            const long long t_begin = pc.t;
             for (int64_t t = cid + static_cast<int64_t>(which) * ncl; t < p.T; t += 2 * ncl, row_iter += 2) {
                 const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
                 const int32_t tok = p.token_ids[t];
@@ -268,7 +272,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 const TokenPre pre = token_pre(p, t, seq);
                 const uint32_t par = row_iter & 1, ph = (row_iter >> 1) & 1;
                 Bcast* bc = bcs + par;
+                if (kPhaseCounters && p.dbg) pc.lap(d_math);
                 support_wait(bar_red + 8 * par, ph);
+                if (kPhaseCounters && p.dbg) pc.lap(d_red);
                 if (kChecked)
                     for (int w = 0; w < NCW; ++w) rf_check(red_tag[par * NCW + w] == t);
                 // CTA partials, warp order
@@ -289,6 +295,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     if (syw != 0.0) Syw += syw * combine_factor(redMy[par * NCW + w], Myw);
                 }
                 double Mc = static_cast<double>(Mw), Myc = static_cast<double>(Myw), Sc = Sw, Tc = Tw, Syc = Syw;
+                if (kPhaseCounters && p.dbg) pc.lap(d_math);
                 if (GX && csize > 1) {
                     const uint32_t xs = row_iter & 3;
                     XSlotG* mine = xg + xs * 8 + rank;
@@ -374,6 +381,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     Mc = static_cast<double>(Mx);
                     Myc = static_cast<double>(Myx);
                 }
+                if (kPhaseCounters && p.dbg) pc.lap(d_x);  // the exchange with the group's peers
                 // the gradient needs lse, k and D only: publish them first; the reference lse
                 // and the KL value (loss and scalars only) follow off the critical path
                 const double lse = kLn2 * (Mc + log2(Sc));
@@ -423,6 +431,13 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 }
             }
             if (rank == 0) part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
+            if (kPhaseCounters && p.dbg) {
+                pc.lap(d_math);
+                atomicAdd(p.dbg + 6, d_red);
+                atomicAdd(p.dbg + 7, d_x);
+                atomicAdd(p.dbg + 8, d_math);
+                atomicAdd(p.dbg + 9, static_cast<unsigned long long>(clock64() - t_begin));
+            }
         }
         __syncwarp();
         tmem_fence_before();
@@ -452,6 +467,12 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         }
         const int jfull = tail_j >= 0 ? tail_j : jmax;
         const size_t thr_off = static_cast<size_t>(slice_begin + tid) * EPV * OES;
+        // phase counters (profiling build): full-wait, stream, park, coef-wait, write, total
+        unsigned long long dph[6] = {0, 0, 0, 0, 0, 0};
+        PhaseClock pcc;
+        pcc.start();
+        const long long t_begin = pcc.t;
+        const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
 
         // copy-in (parking the previous row's e and d chunk by chunk), max, sweep, reduce
         auto stream_row = [&](int64_t t_row, uint32_t row_iter, bool park_prev) -> float {
@@ -468,7 +489,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     }
                 }
                 if (c < nchunks) {
+                    if (dbg) pcc.lap(dph[1]);
                     cons_wait(bar_full + 8 * s, fphase);
+                    if (dbg) pcc.lap(dph[0]);
                     const uint32_t slot = sbase + s * SLOT_BYTES + tid * 16;
                     if (c * VPC + VPC <= jmax) {  // whole chunk inside the slice: plain loads
 #pragma unroll
@@ -561,12 +584,15 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 if (kChecked) red_tag[par * NCW + warp] = t_row;
                 mbar_arrive(bar_red + 8 * par);
             }
+            if (dbg) pcc.lap(dph[1]);
             return C;
         };
 
         auto write_row = [&](int64_t t, uint32_t row_iter, float C) {
             const uint32_t par = row_iter & 1;
+            if (dbg) pcc.lap(dph[4]);
             cons_wait(bar_bc + 8 * par, (row_iter >> 1) & 1);
+            if (dbg) pcc.lap(dph[3]);
             if (kChecked) rf_check(bc_tag[par] == t);
             const Bcast* bc = bcs + par;
             const float f = ex2_approx(C - bc->lseL);
@@ -618,6 +644,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                         reinterpret_cast<float*>(drow)[tokv] = tv;
                 }
             }
+            if (dbg) pcc.lap(dph[4]);
         };
 
         uint32_t it = 0;
@@ -633,6 +660,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     tmem_st4(tmd + 4 * j, ry[j]);
                 }
             }
+            if (dbg) pcc.lap(dph[2]);
             float Cn = 0.f;
             if (tn < p.T) Cn = stream_row(tn, it + 1, true);
             tmem_wait_st();
@@ -640,6 +668,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
             C = Cn;
             t = tn;
             ++it;
+        }
+        if (dbg) {
+            dph[5] = static_cast<unsigned long long>(clock64() - t_begin);
+            for (int q = 0; q < 6; ++q) atomicAdd(p.dbg + q, dph[q]);
         }
     }
     tmem_fence_before();

@@ -1,6 +1,8 @@
-"""Per-phase cycle breakdown of the fused kernel (run on the GPU box):
-    RF_DEBUG_COUNTERS=1 python tools/phase_profile.py [--prompts 32]
-Prints, per consumer warp, where the cycles of one launch went."""
+"""Per-phase cycle breakdown of the fused kernel (run on the GPU box, profiling build):
+    make -C paper_2510_11345_b200 phase
+    RF_LIB_VARIANT=phase RF_DEBUG_COUNTERS=1 python tools/phase_profile.py [--prompts 32] [--kl]
+Prints, per consumer warp, where the cycles of one launch of K2 (or, with --kl, of the
+exact-KL kernel K2kl) went."""
 import argparse
 import ctypes
 import os
@@ -18,15 +20,20 @@ from tests.cases import config  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--prompts", type=int, default=32)
 ap.add_argument("--variant", default="decoupled_ppo")
+ap.add_argument("--kl", action="store_true", help="exact-KL GRPO (K2kl, 4-CTA groups)")
 a = ap.parse_args()
 assert os.environ.get("RF_DEBUG_COUNTERS") == "1"
 wl = S.WORKLOADS["c2"]
 rb = S.make_rank_batch(wl, 0, 1, 42, a.prompts)
 dw = S.DeviceWorkload(rb, wl.vocab, pool_gb=8, device="cuda")
+ref = None
+if a.kl:
+    ref = (torch.randn(dw.pool_rows, (wl.vocab + 7) // 8 * 8, device="cuda") * 2.0).to(torch.bfloat16)[:, :wl.vocab]
 pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_offsets, advantages=dw.advantages,
                    behavior_logp=dw.behavior_logp, row_of_token=dw.row_of_token, prox_logp=dw.prox_logp,
-                   engine_logp=dw.engine_logp, normalization=L.Normalization.global_token)
-op = rf.OffPolicyLoss(config(a.variant), pb, chunk_tokens=min(65536, dw.T))
+                   engine_logp=dw.engine_logp, normalization=L.Normalization.global_token, ref_logits=ref)
+cfg = config("grpo", kl_weight=0.1) if a.kl else config(a.variant)
+op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=min(65536, dw.T))
 lib = _abi.load_library()
 buf = np.zeros(16, dtype=np.uint64)
 for rep in range(3):
@@ -42,7 +49,8 @@ names = ["cons.full_wait", "cons.stream", "cons.park", "cons.coef_wait", "cons.w
          "scal.red_wait", "scal.peer_wait", "scal.math", "scal.total", "prod.empty_wait", "prod.total",
          "scal.post_to_k", "scal.post.lse", "scal.post.token_post"]
 ncta = 148
-print(f"launch {ms:.3f} ms for {op.chunk} tokens -> {op.chunk * 4 * wl.vocab / ms / 1e6:.1f} GB/s")
+bpt = (6 if a.kl else 4) * wl.vocab
+print(f"launch {ms:.3f} ms for {op.chunk} tokens -> {op.chunk * bpt / ms / 1e6:.1f} GB/s ({'K2kl' if a.kl else 'K2'})")
 cons_warps = ncta * 12
 for i, n in enumerate(names):
     div = cons_warps if n.startswith("cons") else (ncta * 2 if n.startswith("scal") else ncta)
