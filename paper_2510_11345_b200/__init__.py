@@ -10,6 +10,7 @@ process that imports only the workload synthesis (``synth``) — e.g. the
 reference arm of bench.py — never loads the product library.
 """
 from ._abi import require_library
+from .batch import PackInfo, Sample, pack_samples  # noqa: F401
 from .losses import (  # noqa: F401
     InvalidArgument,
     LossConfig,
