@@ -79,7 +79,7 @@ def lmhead_dlogits(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch
 
 
 def lmhead_backward(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torch.Tensor, lse: torch.Tensor,
-                    coef: torch.Tensor, *, chunk_vocab: int = 32768, stream=None):
+                    coef: torch.Tensor, *, chunk_vocab: int = 24576, stream=None):
     """The LM-head backward from the loss coefficients, vocabulary chunk by chunk:
 
         dlogits[:, c] = coef·(1[v = tok] − exp(H·W[c]ᵀ − lse))   (tensor-core sweep, bf16)
@@ -109,7 +109,7 @@ def lmhead_backward(hidden: torch.Tensor, w_vocab: torch.Tensor, token_ids: torc
 
 
 def lmhead_loss_and_grad(config, hidden: torch.Tensor, w_vocab: torch.Tensor, batch, stream=None,
-                         check: bool = True, want: str = "dlogits", chunk_vocab: int = 32768):
+                         check: bool = True, want: str = "dlogits", chunk_vocab: int = 24576):
     """The off-policy loss from hidden states, logits never materialised: tensor-core stats
     sweep (lse, sampled logit) -> per-token loss math (``rf_token_loss_from_stats``,
     reference semantics, losses.cpp:262-331) -> either the dlogits sweep (``want="dlogits"``:

@@ -102,6 +102,9 @@ def composed_grads():  # + the backward GEMMs of the materialised dlogits (cuBLA
 
 ms_composed_grads = timed(composed_grads)
 ms_pipeline_grads = timed(lambda: lmhead_loss_and_grad(cfg, H, W, pb, check=False, want="grads"))
+grads_by_chunk = {c: round(timed(lambda: lmhead_loss_and_grad(cfg, H, W, pb, check=False, want="grads",
+                                                               chunk_vocab=c)), 3)
+                  for c in (8192, 16384, 24576, 32768)}
 def peak_gb(fn):
     torch.cuda.synchronize()
     base = torch.cuda.memory_allocated()
@@ -132,6 +135,7 @@ out = {"tokens": T, "vocab": V, "hidden": K, "fused_ms": round(ms_fused, 3),
        "loss_and_dlogits_fused_pipeline_ms": round(ms_pipeline, 3),
        "loss_and_dlogits_cublas_logits_plus_ring_kernel_ms": round(ms_composed, 3),
        "loss_and_grads_fused_pipeline_ms": round(ms_pipeline_grads, 3),
+       "loss_and_grads_fused_ms_by_chunk_vocab": grads_by_chunk,
        "loss_and_grads_composed_ms": round(ms_composed_grads, 3),
        "backward_gemms_cublas_ms": round(ms_bwd_gemms, 3),
        "peak_extra_GB_fused_grads": peak_fused,
