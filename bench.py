@@ -553,7 +553,7 @@ def impl_ours(args, wl, variant):
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step = float(t_local[0]) / args.steps
-    tokens_global = rb.global_tokens if strong else rb.global_tokens
+    tokens_global = rb.global_tokens  # the whole job: every rank's tokens
     value = tokens_global / (ms_step / 1e3)
     step_status = int(op.status.item())
 
