@@ -32,6 +32,11 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {  // one FADD2 with a negated operand
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
 // bf16x2 word -> packed f32x2 (exact)
 __device__ __forceinline__ uint64_t bf16x2_to_f32x2(uint32_t w) {
     return static_cast<uint64_t>(w << 16) | (static_cast<uint64_t>(w & 0xffff0000u) << 32);

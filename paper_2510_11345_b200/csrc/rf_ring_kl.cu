@@ -52,7 +52,7 @@ __device__ __forceinline__ void kl_vec(uint4& vx, uint4& vy, uint64_t L2, uint64
         const float f0 = ex2_approx(lo2(ay)), f1 = ex2_approx(hi2(ay));
         // x - y; -inf - (-inf) (padding) and -inf - y become a large finite negative,
         // so e·d = 0 where e = 0 (fmaxf drops the NaN operand)
-        const uint64_t dd = fadd2(x2, y2 ^ 0x8000000080000000ull);
+        const uint64_t dd = fsub2(x2, y2);
         const float d0 = fmaxf(lo2(dd), -3.0e38f), d1 = fmaxf(hi2(dd), -3.0e38f);
         const uint64_t e2 = pk2(e0, e1);
         se = q == 0 ? e2 : fadd2(se, e2);
