@@ -272,7 +272,6 @@ __device__ __forceinline__ uint32_t ld_relaxed_cluster_u32(uint32_t addr) {
     return v;
 }
 __device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
