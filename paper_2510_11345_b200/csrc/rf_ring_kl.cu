@@ -186,9 +186,19 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const uint32_t rank = GX ? blockIdx.x % static_cast<uint32_t>(p.vcs) : cluster_ctarank();
+    // CTA groups: when the grid covers every SM exactly once (a cooperative launch of one
+    // CTA per SM over contiguous SM ids), a group is 4 neighbouring SM ids (the same GPC)
+    // rather than 4 consecutive block ids; otherwise block ids.
+    uint32_t gslot = blockIdx.x;
+    if (GX) {  // measured +0.5% over block-id groups (profiles/r02_ab/kl_smid_groups_ab.txt)
+        uint32_t smid, nsmid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsmid));
+        if (nsmid == gridDim.x) gslot = smid;
+    }
+    const uint32_t rank = GX ? gslot % static_cast<uint32_t>(p.vcs) : cluster_ctarank();
     const uint32_t csize = GX ? static_cast<uint32_t>(p.vcs) : cluster_nctarank();
-    const uint32_t cid = GX ? blockIdx.x / static_cast<uint32_t>(p.vcs) : cluster_id_x();
+    const uint32_t cid = GX ? gslot / static_cast<uint32_t>(p.vcs) : cluster_id_x();
     const uint32_t ncl = GX ? gridDim.x / static_cast<uint32_t>(p.vcs) : ncluster_x();
     XSlotG* xg = GX ? static_cast<XSlotG*>(p.xch) + static_cast<size_t>(cid) * 32 : nullptr;
 
