@@ -36,6 +36,29 @@ namespace {
 // vectors per packed fp32 partial before the fp64 fold (measured on B200: 2 is +1.2% over 1; 4 gains nothing)
 constexpr int kKlFold = 2;
 
+// Padding of the two rows: a finite bf16 (-1.0e30) instead of -inf, so padded lanes give e = 0 and
+// d = 0 (never 0·inf) without a per-element guard in the sweep.
+constexpr uint32_t kKlPad2 = 0xF14AF14Au;
+constexpr float kKlPadMax = -1.0e29f;  // a slice max at or below this is all padding
+__device__ __forceinline__ uint4 pad_vec_here() {  // volatile: not hoisted out of its branch
+    uint4 v;
+    asm volatile("mov.b32 %0, %4;\n\tmov.b32 %1, %4;\n\tmov.b32 %2, %4;\n\tmov.b32 %3, %4;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "n"(kKlPad2));
+    return v;
+}
+__device__ __forceinline__ void mask_tail_pad(uint4& v, int valid) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        if (e >= valid) {
+            const int wi = e >> 1;
+            w[wi] = (e & 1) ? ((w[wi] & 0x0000ffffu) | (kKlPad2 & 0xffff0000u)) : ((w[wi] & 0xffff0000u) | (kKlPad2 & 0xffffu));
+        }
+    }
+    v = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 // One 8-element vector of x and of y: e (f16x2) replaces x, d = x - y (f16x2)
 // replaces y; packed f32x2 partial sums of e, ey and e·d are accumulated.
 __device__ __forceinline__ void kl_vec(uint4& vx, uint4& vy, uint64_t L2, uint64_t negC2, uint64_t negCy2,
@@ -52,8 +75,10 @@ __device__ __forceinline__ void kl_vec(uint4& vx, uint4& vy, uint64_t L2, uint64
         const float f0 = ex2_approx(lo2(ay)), f1 = ex2_approx(hi2(ay));
         // x - y; -inf - (-inf) (padding) and -inf - y become a large finite negative,
         // so e·d = 0 where e = 0 (fmaxf drops the NaN operand)
+        // x - y.  Padding is the finite kKlPad in both rows (d = 0, e = 0); a genuine -inf logit
+        // makes e·d = 0·inf = NaN, as p·(lp − lq) does in the reference (losses.cpp:127-130).
         const uint64_t dd = fsub2(x2, y2);
-        const float d0 = fmaxf(lo2(dd), -3.0e38f), d1 = fmaxf(hi2(dd), -3.0e38f);
+        const float d0 = lo2(dd), d1 = hi2(dd);
         const uint64_t e2 = pk2(e0, e1);
         se = q == 0 ? e2 : fadd2(se, e2);
         sy = q == 0 ? pk2(f0, f1) : fadd2(sy, pk2(f0, f1));
@@ -518,8 +543,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                             const int j = c * VPC + jj;
                             if (j < NVT) {
                                 const bool ok = j < jmax;
-                                r[j] = ok ? lds128(slot + jj * NCT * 16) : neg_inf_vec_here<true>();
-                                ry[j] = ok ? lds128(slot + CHUNK_BYTES + jj * NCT * 16) : neg_inf_vec_here<true>();
+                                r[j] = ok ? lds128(slot + jj * NCT * 16) : pad_vec_here();
+                                ry[j] = ok ? lds128(slot + CHUNK_BYTES + jj * NCT * 16) : pad_vec_here();
                             }
                         }
                     }
@@ -533,7 +558,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
 #pragma unroll
                     for (int jj = 0; jj < VPC; ++jj) {
                         const int j = c * VPC + jj;
-                        if (j < NVT) r[j] = ry[j] = neg_inf_vec_here<true>();
+                        if (j < NVT) r[j] = ry[j] = pad_vec_here();
                     }
                 }
             }
@@ -541,13 +566,13 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
 #pragma unroll
                 for (int j = 0; j < NVT; ++j)
                     if (j == tail_j) {
-                        mask_tail<true>(r[j], tail_valid);
-                        mask_tail<true>(ry[j], tail_valid);
+                        mask_tail_pad(r[j], tail_valid);
+                        mask_tail_pad(ry[j], tail_valid);
                     }
             }
             const float M = vmax_row(r, NVT), My = vmax_row(ry, NVT);
-            const float C = ((M == -CUDART_INF_F) ? 0.0f : M) * kL2e;
-            const float Cy = ((My == -CUDART_INF_F) ? 0.0f : My) * kL2e;
+            const float C = ((M <= kKlPadMax) ? 0.0f : M) * kL2e;
+            const float Cy = ((My <= kKlPadMax) ? 0.0f : My) * kL2e;
             const uint64_t negC2 = pk2(-C, -C), negCy2 = pk2(-Cy, -Cy);
             // packed fp32 partial sums over kKlFold vectors, folded into fp64
             double S = 0.0, T = 0.0, Sy = 0.0;

@@ -169,3 +169,26 @@ def test_host_api_leaves_default_mempool_alone():
     _host_call(case, config("tis"), 4, L.Normalization.global_token)
     assert cudart.cudaMemPoolGetAttribute(pool, ATTR_RELEASE_THRESHOLD, ctypes.byref(thr)) == 0
     assert thr.value == before
+
+
+@pytest.mark.parametrize("V,kernel", [(32000, "ring"), (151936, "ring"), (4099, "generic")])
+def test_masked_vocabulary_minus_inf_logits(V, kernel):
+    """LLM vocabularies are padded and masked with -inf logits: those entries get p = 0 and a
+    zero dlogit, every other output matches the oracle (whose log-softmax handles -inf the
+    same way, policy.cpp:21-30)."""
+    case = make_case(45, T_seqs=8, G=4, V=V, max_len=6, mapping="A", stale=0.2)
+    rng = np.random.default_rng(45)
+    masked = rng.random(case.logits.shape) < 0.05
+    masked[np.arange(case.T), case.token_ids] = False  # sampled tokens are never masked
+    case.logits = np.where(masked, -np.inf, case.logits)
+    lsm = case.logits - case.logits.max(1, keepdims=True)
+    lp = (lsm - np.log(np.exp(lsm).sum(1, keepdims=True)))[np.arange(case.T), case.token_ids]
+    case.behavior_logp = lp - 0.05
+    case.prox_logp, case.engine_logp = lp - 0.02, lp - 0.06
+    cfg = config("decoupled_ppo", engine_mismatch_cap=2.0)
+    pb = to_device_batch(case, normalization=L.Normalization.global_token)
+    gpu = rf.loss_and_grad(cfg, pb, kernel=kernel)
+    ref = run_oracle(case, cfg, normalization=1)
+    compare(case, cfg, gpu, ref)
+    d = gpu.dlogits.float().cpu().numpy()
+    assert (d[masked] == 0).all() and np.isfinite(d).all()
