@@ -73,8 +73,6 @@ __device__ __forceinline__ void kl_vec(uint4& vx, uint4& vy, uint64_t L2, uint64
         const uint64_t ay = ffma2(y2, L2, negCy2);
         const float e0 = ex2_approx(lo2(a)), e1 = ex2_approx(hi2(a));
         const float f0 = ex2_approx(lo2(ay)), f1 = ex2_approx(hi2(ay));
-        // x - y; -inf - (-inf) (padding) and -inf - y become a large finite negative,
-        // so e·d = 0 where e = 0 (fmaxf drops the NaN operand)
         // x - y.  Padding is the finite kKlPad in both rows (d = 0, e = 0); a genuine -inf logit
         // makes e·d = 0·inf = NaN, as p·(lp − lq) does in the reference (losses.cpp:127-130).
         const uint64_t dd = fsub2(x2, y2);
@@ -293,7 +291,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
             Partials part;
             part.zero();
             uint32_t row_iter = which;
-            unsigned long long d_red = 0, d_x = 0, d_math = 0;  // phase counters (profiling build)
+            unsigned long long d_red = 0, d_x = 0, d_math = 0, d_comb = 0, d_post = 0;  // phase counters (profiling build)
             PhaseClock pc;
             pc.start();
             const long long t_begin = pc.t;
@@ -330,7 +328,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     if (syw != 0.0) Syw += syw * combine_factor(redMy[par * NCW + w], Myw);
                 }
                 double Mc = static_cast<double>(Mw), Myc = static_cast<double>(Myw), Sc = Sw, Tc = Tw, Syc = Syw;
-                if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                if (kPhaseCounters && p.dbg) pc.lap(d_comb);
                 if (GX && csize > 1) {
                     const uint32_t xs = row_iter & 3;
                     XSlotG* mine = xg + xs * 8 + rank;
@@ -452,6 +450,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 }
                 if (kChecked) bc_tag[par] = t;
                 mbar_arrive(bar_bc + 8 * par);
+                if (kPhaseCounters && p.dbg) pc.lap(d_post);
                 const double lseq = kLn2 * (Myc + log2(Syc));
                 const double klv = D - lse + lseq;  // Σ p_v (lp_v - lq_v)
                 const double kl_scaled = __dmul_rn(ks, klv);
@@ -471,6 +470,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 atomicAdd(p.dbg + 6, d_red);
                 atomicAdd(p.dbg + 7, d_x);
                 atomicAdd(p.dbg + 8, d_math);
+                atomicAdd(p.dbg + 12, d_post);
+                atomicAdd(p.dbg + 13, d_comb);
                 atomicAdd(p.dbg + 9, static_cast<unsigned long long>(clock64() - t_begin));
             }
         }

@@ -48,6 +48,8 @@ ms = ev0.elapsed_time(ev1)
 names = ["cons.full_wait", "cons.stream", "cons.park", "cons.coef_wait", "cons.write", "cons.total",
          "scal.red_wait", "scal.peer_wait", "scal.math", "scal.total", "prod.empty_wait", "prod.total",
          "scal.post_to_k", "scal.post.lse", "scal.post.token_post"]
+if a.kl:  # K2kl: slot 12 = exchange done -> coefficient published, slot 13 = combining the warps' partials
+    names[12:15] = ["scal.post_to_bcast", "scal.combine", "-"]
 ncta = 148
 bpt = (6 if a.kl else 4) * wl.vocab
 print(f"launch {ms:.3f} ms for {op.chunk} tokens -> {op.chunk * bpt / ms / 1e6:.1f} GB/s ({'K2kl' if a.kl else 'K2'})")
