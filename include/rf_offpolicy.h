@@ -235,7 +235,9 @@ int32_t rf_last_launch_count(void);
 
 /* Profiling aid: per-phase cycle counters of the fused kernel, accumulated when
  * the process runs with RF_DEBUG_COUNTERS=1 (else returns 0).  Synchronises the
- * device; copies up to n counters into out and optionally resets them. */
+ * device; copies up to n counters into out and optionally resets them.  Words
+ * 0..15 are the phase counters; from word 16 the profiling build stores each
+ * CTA's consumer start / end time (%globaltimer ns), two words per CTA. */
 int32_t rf_debug_counters(uint64_t* out, int32_t n, int32_t reset);
 
 /* ---- experimental: the step before ----

@@ -161,7 +161,7 @@ int ring_clusters(bool ib, bool ob, int kind, int ncw, int nvt, int cs, size_t s
 // exact KL: CTA groups exchanging through L2 (rf_ring_kl.cu GX) fill all 148 SMs
 // where 4-CTA hardware clusters place on 132; RF_KL_GX=0 selects the clusters (A/B).
 constexpr int kKlMaxGroups = 256;
-constexpr size_t kKlSlotBytes = 32 * 40;  // per group: [4 row slots][8 ranks] x sizeof(XSlotG)
+constexpr size_t kKlSlotBytes = rf::kKlGroupXchBytes;  // per group (rf_kernels.h)
 bool kl_groups_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("RF_KL_GX");
@@ -172,14 +172,27 @@ bool kl_groups_enabled() {
 
 int generic_grid(int64_t T) { return static_cast<int>(std::min<int64_t>(T, rf::kGenericMaxGrid)); }
 
+// partial rows: one per token for the lag kernels (per CTA / per sequence elsewhere),
+// plus the finalize's scratch rows
 int64_t partial_rows(const rf_batch* b) {
-    return std::max<int64_t>(std::max<int64_t>(rf::kGenericMaxGrid, b->num_seqs), (b->num_tokens + 255) / 256);
+    return std::max<int64_t>(std::max<int64_t>(rf::kGenericMaxGrid, b->num_seqs), b->num_tokens) +
+           rf::kFinalizeBlocks;
+}
+
+// Lag kernels: dynamic row claims (default) or the static cid + k·ncl walk (RF_ROW_SCHED=static, A/B).
+bool dynamic_rows_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("RF_ROW_SCHED");
+        return !(e && std::string(e) == "static");
+    }();
+    return on;
 }
 
 struct WsLayout {
     double* partials = nullptr;
     double *lse = nullptr, *lp = nullptr, *coef = nullptr, *klx = nullptr, *lseq = nullptr;
     void* xch = nullptr;  // exact-KL CTA-group exchange slots
+    unsigned int* row_ctr = nullptr;  // lag kernels: dynamic row counter
     size_t bytes = 0;
 };
 
@@ -194,6 +207,7 @@ WsLayout ws_layout(const rf_loss_config* c, const rf_batch* b, void* base) {
     };
     w.partials = take(static_cast<size_t>(partial_rows(b)) * RF_NUM_SCALARS * sizeof(double));
     if (c->variant == RF_GRPO && c->kl_weight > 0.0) w.xch = take(kKlMaxGroups * kKlSlotBytes);
+    w.row_ctr = reinterpret_cast<unsigned int*>(take(256));
     if (c->aggregation == RF_SEQUENCE_PRODUCT) {
         const size_t T = static_cast<size_t>(b->num_tokens);
         w.lse = take(T * 8);
@@ -218,8 +232,8 @@ unsigned long long* debug_counters() {
     if (enabled < 0) {
         const char* e = std::getenv("RF_DEBUG_COUNTERS");
         enabled = (e && e[0] == '1') ? 1 : 0;
-        if (enabled && cudaMalloc(&buf, 16 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(buf, 0, 16 * sizeof(unsigned long long));
+        if (enabled && cudaMalloc(&buf, rf::kDbgWords * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(buf, 0, rf::kDbgWords * sizeof(unsigned long long));
         else
             buf = nullptr;
     }
@@ -316,10 +330,10 @@ int32_t rf_last_launch_count(void) { return g_last_launches; }
 int32_t rf_debug_counters(uint64_t* out, int32_t n, int32_t reset) {
     unsigned long long* buf = debug_counters();
     if (!buf || !out || n <= 0) return 0;
-    n = n > 16 ? 16 : n;
+    n = n > rf::kDbgWords ? rf::kDbgWords : n;
     cudaDeviceSynchronize();
     cudaMemcpy(out, buf, static_cast<size_t>(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost);
-    if (reset) cudaMemset(buf, 0, 16 * sizeof(unsigned long long));
+    if (reset) cudaMemset(buf, 0, rf::kDbgWords * sizeof(unsigned long long));
     return n;
 }
 
@@ -479,6 +493,13 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
                 if (cudaMemsetAsync(ws.xch, 0, static_cast<size_t>(kKlMaxGroups) * kKlSlotBytes, s) != cudaSuccess)
                     return RF_ERR_CUDA;
             }
+            // the lag kernels write one partial row per token: scalars independent of which
+            // cluster took which row (bit-identical with static and dynamic row claims)
+            p.row_ctr = nullptr;
+            if (dynamic_rows_enabled()) {
+                p.row_ctr = ws.row_ctr;
+                if (cudaMemsetAsync(ws.row_ctr, 0, sizeof(unsigned int), s) != cudaSuccess) return RF_ERR_CUDA;
+            }
             int ncl = static_cast<int>(std::min<int64_t>(b->num_tokens, maxc));
             cudaError_t e = g.kind == 3 ? rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s)
                                         : rf::launch_ring_lag(p, ib, ob, g.ncw, g.nvt, g.cs, ncl, g.smem, s);
@@ -492,7 +513,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
                 e = rf::launch_ring_kl(p, ob, g.nvt, g.cs, ncl, g.smem, s);
             }
             if (e != cudaSuccess) return RF_ERR_CUDA;
-            nparts = 2 * ncl;  // lag kernels: one partial row per scalar warp
+            nparts = b->num_tokens;  // lag kernels: one partial row per token
         } else {
             const int grid = generic_grid(b->num_tokens);
             if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
@@ -503,7 +524,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
     if (rf::launch_finalize(ws.partials, nparts, o->scalars, b->seq_of_token, b->seq_offsets, b->num_tokens,
                             b->num_seqs, o->device_status, s) != cudaSuccess)
         return RF_ERR_CUDA;
-    g_last_launches += 1;
+    g_last_launches += rf::finalize_launches(nparts);
     return RF_OK;
 }
 
@@ -593,7 +614,7 @@ rf_status rf_token_loss_from_stats(const rf_loss_config* c, const rf_batch* b, c
     if (rf::launch_finalize(ws.partials, (b->num_tokens + 255) / 256, o->scalars, b->seq_of_token, b->seq_offsets,
                             b->num_tokens, b->num_seqs, o->device_status, s) != cudaSuccess)
         return RF_ERR_CUDA;
-    g_last_launches = 2;
+    g_last_launches = 1 + rf::finalize_launches((b->num_tokens + 255) / 256);
     return RF_OK;
 }
 

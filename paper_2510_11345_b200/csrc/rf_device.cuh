@@ -62,6 +62,9 @@ struct KParams {
     // exact-KL kernel with CTA groups exchanging through L2 instead of a hardware cluster
     void* xch;                 // [groups][4 row slots][8 ranks] exchange slots (workspace)
     int32_t vcs;               // CTAs per group (0 = hardware cluster)
+    // lag kernels: per-launch row counter (zeroed before the launch) for dynamic row
+    // claims; nullptr = static rows cid + k·ncl
+    unsigned int* row_ctr;
 };
 
 // Per-phase cycle counters are compiled in only for the profiling build
@@ -83,6 +86,26 @@ constexpr bool kPhaseCounters = RF_PHASE_COUNTERS != 0;
 constexpr bool kChecked = RF_CHECKED != 0;
 __device__ __forceinline__ void rf_check(bool ok) {
     if (RF_CHECKED && !ok) __trap();
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Profiling build: per-CTA consumer {start ns, end ns (%globaltimer), %smid, rows} in
+// dbg[kDbgCtaTimes + 4·cta + {0..3}].
+constexpr int kDbgCtaTimes = 16;
+constexpr int kDbgWords = kDbgCtaTimes + 4 * 1024;
+__device__ __forceinline__ void dbg_cta_end(unsigned long long* dbg, uint32_t rows) {
+    if (blockIdx.x >= 1024) return;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* w = dbg + kDbgCtaTimes + 4 * blockIdx.x;
+    w[1] = global_ns();
+    w[2] = smid;
+    w[3] = rows;
 }
 
 // Debug phase timer: accumulates clock64 deltas into a per-thread slot array.
@@ -396,10 +419,12 @@ struct TokenResult {
 };
 
 // po/tp: decoupled_ppo prox/behaviour and theta/prox ratios; logp: lp (token) or
-// logp_sum (sequence).  Flags per include/rf_offpolicy.h.
+// logp_sum (sequence).  Flags per include/rf_offpolicy.h.  VARIANT >= 0 fixes the
+// variant at compile time (a kernel that serves one variant only, e.g. exact-KL GRPO).
+template <int VARIANT = -1>
 __device__ __forceinline__ void variant_math(const KParams& p, double r, double A, double po, double tp,
                                              double logp, double& value, double& gw, uint32_t& flags) {
-    switch (p.variant) {
+    switch (VARIANT >= 0 ? VARIANT : p.variant) {
         case RF_PPO:
         case RF_GRPO: {
             const double c = clipd(r, 1.0 - p.clip_eps, 1.0 + p.clip_eps);
@@ -490,16 +515,20 @@ __device__ __forceinline__ TokenPre token_pre(const KParams& p, int64_t t, int64
     return q;
 }
 
-// The lp-dependent half (losses.cpp:264-320).
+// The lp-dependent half (losses.cpp:264-320).  On the scalar lane's critical path:
+// with VARIANT fixed, no other variant's work (e.g. decoupled_ppo's second exp) is
+// evaluated and discarded.
+template <int VARIANT = -1>
 __device__ __forceinline__ TokenResult token_post(const KParams& p, const TokenPre& q, double lp) {
     TokenResult o;
     o.flags = q.flags;
     const double r = exp(lp - q.b);
     o.ratio = r;
     if (!isfinite(r)) o.flags |= RF_FLAG_NONFINITE;
-    const double tp = (p.variant == RF_DECOUPLED_PPO) ? exp(lp - q.lq) : 0.0;
+    const int variant = VARIANT >= 0 ? VARIANT : p.variant;
+    const double tp = (variant == RF_DECOUPLED_PPO) ? exp(lp - q.lq) : 0.0;
     double value, gw;
-    variant_math(p, r, q.A, q.po, tp, lp, value, gw, o.flags);
+    variant_math<VARIANT>(p, r, q.A, q.po, tp, lp, value, gw, o.flags);
     const double sm = __dmul_rn(q.scale, q.m);
     o.k = __dmul_rn(p.grad_sign, __dmul_rn(sm, gw));
     o.loss = __dmul_rn(sm, value);
@@ -528,6 +557,14 @@ struct Partials {
         v[RF_SCALAR_MISMATCH] += (r.flags & RF_FLAG_MISMATCH_CAPPED) ? 1.0 : 0.0;
         v[RF_SCALAR_KL] += kl_scaled;
         v[RF_SCALAR_COEF_ABS] += fabs(r.k);
+    }
+    // One token's row of contributions (the lag kernels write one row per token, so the
+    // scalars do not depend on which cluster processed which row).
+    __device__ __forceinline__ static void store_token(double* dst, const TokenResult& r, double kl_scaled) {
+        Partials q;
+        q.zero();
+        q.add_token(r, kl_scaled);
+        q.store(dst);
     }
     __device__ __forceinline__ void store(double* dst) const {
 #pragma unroll

@@ -482,9 +482,37 @@ cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double
     return cudaGetLastError();
 }
 
+// Stage 1 of a long partial-row reduction (one row per token from the lag kernels):
+// block b sums the contiguous rows [b·R, (b+1)·R) in a fixed order into row b of `out`.
+__global__ void reduce_rows_kernel(const double* __restrict__ partials, int64_t n, double* __restrict__ out) {
+    __shared__ double sh[256];
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = static_cast<int64_t>(blockIdx.x) * per, hi = min(n, lo + per);
+    for (int j = 0; j < RF_NUM_SCALARS; ++j) {
+        double a = 0.0;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += 256) a += partials[i * RF_NUM_SCALARS + j];
+        sh[threadIdx.x] = a;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[static_cast<size_t>(blockIdx.x) * RF_NUM_SCALARS + j] = sh[0];
+        __syncthreads();
+    }
+}
+
+int finalize_launches(int64_t n) { return n > kFinalizeDirectRows ? 2 : 1; }
+
 cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, const int32_t* seq_of_token,
                             const int64_t* seq_offsets, int64_t num_tokens, int64_t num_seqs, int32_t* status,
                             cudaStream_t st) {
+    if (n > kFinalizeDirectRows) {  // scratch rows [n, n + kFinalizeBlocks) follow the partials
+        double* mid = const_cast<double*>(partials) + static_cast<size_t>(n) * RF_NUM_SCALARS;
+        reduce_rows_kernel<<<kFinalizeBlocks, 256, 0, st>>>(partials, n, mid);
+        partials = mid;
+        n = kFinalizeBlocks;
+    }
     finalize_kernel<<<1, 256, 0, st>>>(partials, n, scalars, seq_of_token, seq_offsets, num_tokens, num_seqs, status);
     return cudaGetLastError();
 }

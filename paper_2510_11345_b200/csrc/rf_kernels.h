@@ -35,8 +35,11 @@ constexpr size_t kRingLagBarrierBytes = 48;
 // 13: 4-CTA groups at V = 151,936 (larger groups lose: 5-CTA groups at NVT 10 -12%, 7-CTA at NVT 8 -40%,
 // profiles/r02_ab/kl_group_and_exchange_ab.txt)
 constexpr int kRingNvtKL[3] = {4, 10, 13};
+// exact-KL CTA groups (GX): per group [4 row slots][8 ranks] x 40-byte exchange slots, then
+// the group's row-claim ring (kRowQ 64-bit words); zeroed before every launch
+constexpr size_t kKlGroupXchBytes = 32 * 40 + 64;
 // [4][8] 40-byte exchange slots + 5 x [2][NCW] partials + broadcast (+ checked-build row tags)
-constexpr size_t kRingKLTailBytes = RF_CHECKED ? 2176 + 2 * 16 * 8 + 16 : 2176;
+constexpr size_t kRingKLTailBytes = RF_CHECKED ? 2304 + 2 * 16 * 8 + 16 : 2304;
 cudaError_t launch_ring_kl(const KParams& p, bool out_bf16, int nvt, int cs, int nclusters, size_t smem,
                            cudaStream_t st);
 cudaError_t ring_kl_max_clusters(bool out_bf16, int nvt, int cs, size_t smem, int* out);
@@ -51,6 +54,11 @@ cudaError_t launch_ring_lag(const KParams& p, bool in_bf16, bool out_bf16, int n
 cudaError_t ring_lag_max_clusters(bool in_bf16, bool out_bf16, int ncw, int nvt, int cs, size_t smem, int* out);
 constexpr int kGenericThreads = 256;
 constexpr int kGenericMaxGrid = 148 * 8;
+// finalize: up to this many partial rows in one block; more (one row per token from the
+// lag kernels) first go through kFinalizeBlocks fixed-range block sums, written into the
+// kFinalizeBlocks scratch rows that follow the partials
+constexpr int64_t kFinalizeDirectRows = 4096;
+constexpr int kFinalizeBlocks = 148;
 
 cudaError_t launch_generic(const KParams& p, bool in_bf16, bool out_bf16, int grid, cudaStream_t st);
 // K2w (rf_stream.cu): dlogits from per-token coef + lse (needs p.row_vecs, ring-compatible layout)
@@ -60,6 +68,7 @@ cudaError_t launch_stream_stats(const KParams& p, bool in_bf16, cudaStream_t st)
 cudaError_t launch_seq(const KParams& p, int64_t seq_begin, int64_t nseq, double* coef, cudaStream_t st);
 cudaError_t launch_token_loss(const KParams& p, const double* lse, const float* xtok, cudaStream_t st);
 // K3: scalar reduce + the empty-trajectory check over the sequences this call spans
+int finalize_launches(int64_t n);
 cudaError_t launch_finalize(const double* partials, int64_t n, double* scalars, const int32_t* seq_of_token,
                             const int64_t* seq_offsets, int64_t num_tokens, int64_t num_seqs, int32_t* status,
                             cudaStream_t st);

@@ -118,6 +118,63 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint4& a) {
         : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Row queue: the rows a CTA processes, in order.  Entry k (k-th row of this CTA) is
+// rowq[k % kRowQ] (a token index, or -1 = no more rows), published by completing
+// phase k / kRowQ of the count-1 mbarrier bar_rq[k % kRowQ]; the producer, the
+// consumer warps and the scalar warps all read it with rq_get.  A cluster's rank-0
+// producer publishes into every CTA of the cluster (DSMEM store + remote arrive), so
+// all ranks walk the same rows.  Rows are claimed dynamically from a per-launch
+// counter (the first row of each cluster is its id, later rows ncl + atomicAdd), so a
+// cluster on a faster SM pair takes more rows than one on a slower pair instead of
+// every cluster getting T / ncl rows (measured per-cluster row times differ by up to
+// 6% in K2 and 18% in the 4-CTA exact-KL groups: profiles/r02_ncu/*_cta_spans.txt).
+// Safe as long as no reader trails the publisher by kRowQ rows (the ring of
+// TMA slots and the one-row lag bound the distance to ~3).
+constexpr uint32_t kRowQ = 8;
+constexpr uint32_t kRowLookahead = 2;  // rows published ahead of the row being loaded
+
+__device__ __forceinline__ int64_t rq_get(const int64_t* rowq, uint32_t bar_rq, uint32_t k) {
+    const uint32_t bar = bar_rq + 8 * (k % kRowQ), par = (k / kRowQ) & 1;
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(par), "r"(1000000u)
+            : "memory");
+    } while (!ok);
+    return *reinterpret_cast<const volatile int64_t*>(rowq + (k % kRowQ));
+}
+
+// Publish entry k = t in CTA `dst` of the cluster (dst == own rank: a local store + arrive).
+__device__ __forceinline__ void rq_put(int64_t* rowq, uint32_t bar_rq, uint32_t k, int64_t t, uint32_t dst,
+                                       uint32_t own) {
+    const uint32_t slot = smem_u32(rowq + (k % kRowQ)), bar = bar_rq + 8 * (k % kRowQ);
+    if (dst == own) {
+        asm volatile("st.shared.s64 [%0], %1;" ::"r"(slot), "l"(t) : "memory");
+        mbar_arrive(bar);
+    } else {
+        asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(mapa(slot, dst)), "l"(t) : "memory");
+        mbar_arrive_remote(mapa(bar, dst));
+    }
+}
+
+// The k-th row of cluster `cid` out of `ncl` (dynamic: k = 0 is cid, later rows are
+// claimed from the launch's counter; static: cid + k·ncl), -1 past the end.
+__device__ __forceinline__ int64_t rq_claim(const KParams& p, uint32_t k, uint32_t cid, uint32_t ncl) {
+    int64_t t;
+    if (k == 0)
+        t = cid;
+    else if (p.row_ctr)
+        t = static_cast<int64_t>(ncl) + atomicAdd(p.row_ctr, 1u);
+    else
+        t = static_cast<int64_t>(cid) + static_cast<int64_t>(k) * ncl;
+    return t < p.T ? t : -1;
+}
+
 }  // namespace
 
 }  // namespace rf

@@ -204,7 +204,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
     };
     Bcast* bcs = reinterpret_cast<Bcast*>(tail + 1280 + 64 * NCW);  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bcs + 2);
-    int64_t* red_tag = reinterpret_cast<int64_t*>(tail + 2176);  // [2][NCW] checked build: row of each partial
+    static_assert(1280 + 64 * NCW + 2 * sizeof(Bcast) + 4 <= 2176, "tail layout");
+    int64_t* rowq = reinterpret_cast<int64_t*>(tail + 2176);      // [kRowQ] row queue (rf_lag_common.cuh)
+    const uint32_t bar_rq = smem_u32(tail + 2240);                 // [kRowQ] its mbarriers
+    int64_t* red_tag = reinterpret_cast<int64_t*>(tail + 2304);  // [2][NCW] checked build: row of each partial
     int64_t* bc_tag = red_tag + 32;                               // [2] checked build: row of each broadcast
 
     const int tid = threadIdx.x;
@@ -223,7 +226,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
     const uint32_t csize = GX ? static_cast<uint32_t>(p.vcs) : cluster_nctarank();
     const uint32_t cid = GX ? gslot / static_cast<uint32_t>(p.vcs) : cluster_id_x();
     const uint32_t ncl = GX ? gridDim.x / static_cast<uint32_t>(p.vcs) : ncluster_x();
-    XSlotG* xg = GX ? static_cast<XSlotG*>(p.xch) + static_cast<size_t>(cid) * 32 : nullptr;
+    static_assert(sizeof(XSlotG) == 40 && kKlGroupXchBytes == 32 * 40 + 8 * kRowQ, "group exchange layout");
+    XSlotG* xg = GX ? reinterpret_cast<XSlotG*>(static_cast<uint8_t*>(p.xch) + static_cast<size_t>(cid) * kKlGroupXchBytes)
+                    : nullptr;
 
     if (tid == 0) {
         for (int s = 0; s < nslots; ++s) {
@@ -235,6 +240,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
             mbar_init(bar_bc + 8 * q, 1);
         }
         for (int q = 0; q < 32; ++q) xslot[q].seq = 0u;
+        for (uint32_t q = 0; q < kRowQ; ++q) mbar_init(bar_rq + 8 * q, 1);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -261,7 +267,52 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 const uint64_t pol = l2_evict_first_policy();
                 int s = 0;
                 uint32_t phase = 0, uses = 0;
-                for (int64_t t = cid; t < p.T; t += ncl) {
+                // rank 0 claims the group's rows; a hardware cluster's ranks get them through
+                // DSMEM (rq_put), a CTA group's through the group's claim ring in L2: one 64-bit
+                // word per entry, (k + 1) << 32 | (t + 1), single-copy atomic, so no fence
+                unsigned long long* claim =
+                    GX ? reinterpret_cast<unsigned long long*>(xg + 32) : nullptr;  // [kRowQ] after the slots
+                uint32_t pub = 0;
+                bool ended = false;
+                auto publish_upto = [&](uint32_t upto, bool block) {
+                    while (!ended && pub < upto) {
+                        int64_t tq;
+                        if (rank == 0) {
+                            tq = rq_claim(p, pub, cid, ncl);
+                            if (GX) {
+                                st_relaxed_gpu_u64(claim + pub % kRowQ,
+                                                   (static_cast<unsigned long long>(pub + 1) << 32) |
+                                                       static_cast<uint32_t>(tq + 1));
+                                rq_put(rowq, bar_rq, pub, tq, rank, rank);
+                            } else {
+                                for (uint32_t q = 0; q < csize; ++q) rq_put(rowq, bar_rq, pub, tq, q, rank);
+                            }
+                        } else if (GX) {
+                            unsigned long long w;
+                            while (((w = ld_relaxed_gpu_u64(claim + pub % kRowQ)) >> 32) != pub + 1) {
+                                if (!block) return;  // look-ahead: the leader has not claimed it yet
+                                __nanosleep(64);
+                            }
+                            tq = static_cast<int64_t>(static_cast<uint32_t>(w)) - 1;
+                            rq_put(rowq, bar_rq, pub, tq, rank, rank);
+                        } else {
+                            return;  // a cluster's rank 0 publishes into this CTA
+                        }
+                        ++pub;
+                        if (tq < 0) {  // the end, twice: the other scalar warp reads the entry after it
+                            if (GX)
+                                rq_put(rowq, bar_rq, pub, -1, rank, rank);
+                            else
+                                for (uint32_t q = 0; q < csize; ++q) rq_put(rowq, bar_rq, pub, -1, q, rank);
+                            ++pub;
+                            ended = true;
+                        }
+                    }
+                };
+                for (uint32_t k = 0;; ++k) {
+                    publish_upto(k + 1, true);
+                    const int64_t t = rq_get(rowq, bar_rq, k);
+                    if (t < 0) break;
                     const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
                     const uint8_t* src = reinterpret_cast<const uint8_t*>(p.logits) + (row * p.row_stride) * 2 +
                                          static_cast<size_t>(slice_begin) * 16;
@@ -282,20 +333,22 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                             if (uses > static_cast<uint32_t>(nslots)) phase ^= 1;
                         }
                     }
+                    publish_upto(k + 1 + kRowLookahead, false);
                 }
             }
             __syncwarp();
-        } else if ((warp == NCW + 1 || warp == NCW + 2) && lane == 0) {
+        } else if (warp == NCW + 1 || warp == NCW + 2) {
             // --------------------------------- scalar ---------------------------------
+            // The whole warp combines the consumer warps' partials (one warp per lane, shuffle
+            // trees); lane 0 alone runs the exchange, the token math and the broadcast.
             const uint32_t which = static_cast<uint32_t>(warp - NCW - 1);
-            Partials part;
-            part.zero();
-            uint32_t row_iter = which;
             unsigned long long d_red = 0, d_x = 0, d_math = 0, d_comb = 0, d_post = 0;  // phase counters (profiling build)
             PhaseClock pc;
             pc.start();
             const long long t_begin = pc.t;
-            for (int64_t t = cid + static_cast<int64_t>(which) * ncl; t < p.T; t += 2 * ncl, row_iter += 2) {
+            for (uint32_t row_iter = which;; row_iter += 2) {
+                const int64_t t = rq_get(rowq, bar_rq, row_iter);  // all lanes
+                if (t < 0) break;
                 const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
                 const int32_t tok = p.token_ids[t];
                 const bool tok_ok = tok >= 0 && tok < p.V;
@@ -308,25 +361,31 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
                 support_wait(bar_red + 8 * par, ph);
                 if (kPhaseCounters && p.dbg) pc.lap(d_red);
-                if (kChecked)
-                    for (int w = 0; w < NCW; ++w) rf_check(red_tag[par * NCW + w] == t);
-                // CTA partials, warp order
-                float Mw = -CUDART_INF_F, Myw = -CUDART_INF_F;
-                for (int w = 0; w < NCW; ++w) {
-                    Mw = fmaxf(Mw, redM[par * NCW + w]);
-                    Myw = fmaxf(Myw, redMy[par * NCW + w]);
+                if (kChecked && lane < NCW) rf_check(red_tag[par * NCW + lane] == t);
+                // CTA partials: lane w holds consumer warp w's, fixed butterfly trees (lane 0's
+                // result is the one used; the same on every launch)
+                const bool has = lane < NCW;
+                const float m_l = has ? redM[par * NCW + lane] : -CUDART_INF_F;
+                const float my_l = has ? redMy[par * NCW + lane] : -CUDART_INF_F;
+                const double s_l = has ? redS[par * NCW + lane] : 0.0;
+                const double t_l = has ? redT[par * NCW + lane] : 0.0;
+                const double sy_l = has ? redSy[par * NCW + lane] : 0.0;
+                float Mw = m_l, Myw = my_l;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
+                    Myw = fmaxf(Myw, __shfl_xor_sync(0xffffffffu, Myw, o));
                 }
-                double Sw = 0.0, Tw = 0.0, Syw = 0.0;
-                for (int w = 0; w < NCW; ++w) {
-                    const double sw = redS[par * NCW + w];
-                    if (sw != 0.0) {
-                        const double f = combine_factor(redM[par * NCW + w], Mw);
-                        Sw += sw * f;
-                        Tw += redT[par * NCW + w] * f;
-                    }
-                    const double syw = redSy[par * NCW + w];
-                    if (syw != 0.0) Syw += syw * combine_factor(redMy[par * NCW + w], Myw);
+                const double f_l = (s_l != 0.0) ? combine_factor(m_l, Mw) : 0.0;
+                double Sw = s_l * f_l, Tw = t_l * f_l;
+                double Syw = (sy_l != 0.0) ? sy_l * combine_factor(my_l, Myw) : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    Sw += __shfl_xor_sync(0xffffffffu, Sw, o);
+                    Tw += __shfl_xor_sync(0xffffffffu, Tw, o);
+                    Syw += __shfl_xor_sync(0xffffffffu, Syw, o);
                 }
+                if (lane == 0) {
                 double Mc = static_cast<double>(Mw), Myc = static_cast<double>(Myw), Sc = Sw, Tc = Tw, Syc = Syw;
                 if (kPhaseCounters && p.dbg) pc.lap(d_comb);
                 if (GX && csize > 1) {
@@ -429,7 +488,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     tr.flags = RF_FLAG_NONFINITE | RF_FLAG_ZERO_COEF;
                 } else {
                     lp = static_cast<double>(x_tok) - lse;
-                    tr = token_post(p, pre, lp);
+                    tr = token_post<RF_GRPO>(p, pre, lp);  // the exact-KL path is GRPO only
                     if (tr.flags & RF_FLAG_NONFINITE) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
                 }
                 const double ks = pre.scale;
@@ -461,11 +520,12 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
                     if (p.token_coef) p.token_coef[t] = tr.k;
                     if (p.token_loss) p.token_loss[t] = tr.loss;
                     if (p.token_flags) p.token_flags[t] = static_cast<uint8_t>(tr.flags);
-                    part.add_token(tr, kl_scaled);
+                    Partials::store_token(p.partials + static_cast<size_t>(t) * RF_NUM_SCALARS, tr, kl_scaled);
                 }
+                }  // lane 0
+                __syncwarp();
             }
-            if (rank == 0) part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
-            if (kPhaseCounters && p.dbg) {
+            if (kPhaseCounters && p.dbg && lane == 0) {
                 pc.lap(d_math);
                 atomicAdd(p.dbg + 6, d_red);
                 atomicAdd(p.dbg + 7, d_x);
@@ -509,6 +569,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         pcc.start();
         const long long t_begin = pcc.t;
         const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
+        if (dbg && warp == 0 && blockIdx.x < 1024) p.dbg[kDbgCtaTimes + 4 * blockIdx.x] = global_ns();
 
         // copy-in (parking the previous row's e and d chunk by chunk), max, sweep, reduce
         auto stream_row = [&](int64_t t_row, uint32_t row_iter, bool park_prev) -> float {
@@ -684,12 +745,12 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         };
 
         uint32_t it = 0;
-        int64_t t = cid;
+        int64_t t = rq_get(rowq, bar_rq, 0);
         float C = 0.f;
-        if (t < p.T) C = stream_row(t, 0, false);
-        while (t < p.T) {
-            const int64_t tn = t + ncl;
-            if (tn >= p.T) {  // last row: park it whole
+        if (t >= 0) C = stream_row(t, 0, false);
+        while (t >= 0) {
+            const int64_t tn = rq_get(rowq, bar_rq, it + 1);
+            if (tn < 0) {  // last row: park it whole
 #pragma unroll
                 for (int j = 0; j < NVT; ++j) {
                     tmem_st4(tm + 4 * j, r[j]);
@@ -698,7 +759,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
             }
             if (dbg) pcc.lap(dph[2]);
             float Cn = 0.f;
-            if (tn < p.T) Cn = stream_row(tn, it + 1, true);
+            if (tn >= 0) Cn = stream_row(tn, it + 1, true);
             tmem_wait_st();
             write_row(t, it, C);
             C = Cn;
@@ -708,6 +769,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         if (dbg) {
             dph[5] = static_cast<unsigned long long>(clock64() - t_begin);
             for (int q = 0; q < 6; ++q) atomicAdd(p.dbg + q, dph[q]);
+            if (warp == 0) dbg_cta_end(p.dbg, it);
         }
     }
     tmem_fence_before();

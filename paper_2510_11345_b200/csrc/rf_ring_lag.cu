@@ -77,6 +77,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
     };
     Bcast* bcs = reinterpret_cast<Bcast*>(tail + 512 + 24 * NCW + ((24 * NCW) % 8 ? 4 : 0));  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bcs + 2);
+    static_assert(512 + 24 * NCW + 4 + 2 * sizeof(Bcast) + 4 <= 896, "tail layout");
+    int64_t* rowq = reinterpret_cast<int64_t*>(tail + 896);       // [kRowQ] row queue (rf_lag_common.cuh)
+    const uint32_t bar_rq = smem_u32(tail + 960);                  // [kRowQ] its mbarriers
     int64_t* red_tag = reinterpret_cast<int64_t*>(tail + 1088);  // [2][NCW] checked build: row of each partial
     int64_t* bc_tag = red_tag + 32;                               // [2] checked build: row of each broadcast
 
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             xslot[q].S = 0.0;  // tag 0 in both words: never a live use
             xslot[q].seq = 0u;
         }
+        for (uint32_t q = 0; q < kRowQ; ++q) mbar_init(bar_rq + 8 * q, 1);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -131,7 +135,26 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
             PhaseClock pc;
             pc.start();
             const long long t_begin = pc.t;
-            for (int64_t t = cid; t < p.T; t += ncl) {
+            // rank 0 claims the cluster's rows and publishes them to every rank's row queue,
+            // kRowLookahead rows ahead of the row it is loading
+            uint32_t pub = 0;
+            bool ended = false;
+            auto publish_upto = [&](uint32_t upto) {
+                while (rank == 0 && !ended && pub < upto) {
+                    const int64_t tq = rq_claim(p, pub, cid, ncl);
+                    for (uint32_t q = 0; q < csize; ++q) rq_put(rowq, bar_rq, pub, tq, q, rank);
+                    ++pub;
+                    if (tq < 0) {  // the end, twice: the other scalar warp reads the entry after it
+                        for (uint32_t q = 0; q < csize; ++q) rq_put(rowq, bar_rq, pub, -1, q, rank);
+                        ++pub;
+                        ended = true;
+                    }
+                }
+            };
+            for (uint32_t k = 0;; ++k) {
+                publish_upto(k + 1);
+                const int64_t t = rq_get(rowq, bar_rq, k);
+                if (t < 0) break;
                 const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
                 const uint8_t* src = reinterpret_cast<const uint8_t*>(p.logits) + (row * p.row_stride) * IES +
                                      static_cast<size_t>(slice_begin) * 16;
@@ -152,6 +175,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                         if (uses > static_cast<uint32_t>(nslots)) phase ^= 1;
                     }
                 }
+                publish_upto(k + 1 + kRowLookahead);
             }
             if (kPhaseCounters && p.dbg) {
                 dt = static_cast<unsigned long long>(clock64() - t_begin);
@@ -168,14 +192,13 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         // 32-lane shuffle-tree combine measured no faster).
         if (lane == 0) {
             const uint32_t which = static_cast<uint32_t>(warp - NCW - 1);
-            Partials part;
-            part.zero();
-            uint32_t row_iter = which;
             unsigned long long d_red = 0, d_x = 0, d_math = 0, d_post = 0;
             PhaseClock pc;
             pc.start();
             const long long t_begin = pc.t;
-            for (int64_t t = cid + static_cast<int64_t>(which) * ncl; t < p.T; t += 2 * ncl, row_iter += 2) {
+            for (uint32_t row_iter = which;; row_iter += 2) {
+                const int64_t t = rq_get(rowq, bar_rq, row_iter);
+                if (t < 0) break;
                 // issue the per-token loads before waiting
                 const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
                 const int32_t tok = p.token_ids[t];
@@ -258,11 +281,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     if (p.token_coef) p.token_coef[t] = tr.k;
                     if (p.token_loss) p.token_loss[t] = tr.loss;
                     if (p.token_flags) p.token_flags[t] = static_cast<uint8_t>(tr.flags);
-                    part.add_token(tr, 0.0);
+                    Partials::store_token(p.partials + static_cast<size_t>(t) * RF_NUM_SCALARS, tr, 0.0);
                 }
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
             }
-            if (rank == 0) part.store(p.partials + (2 * static_cast<size_t>(cid) + which) * RF_NUM_SCALARS);
             if (kPhaseCounters && p.dbg) {
                 atomicAdd(p.dbg + 6, d_red);
                 atomicAdd(p.dbg + 7, d_x);
@@ -306,6 +328,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         pcc.start();
         const long long t_begin = pcc.t;
         const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
+        if (dbg && warp == 0 && blockIdx.x < 1024) p.dbg[kDbgCtaTimes + 4 * blockIdx.x] = global_ns();
 
         // copy-in + max + exp sweep + CTA reduction of row t into r[]; returns C_t.
         auto stream_row = [&](int64_t t_row, uint32_t row_iter, bool park_prev) -> float {
@@ -466,19 +489,19 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         };
 
         uint32_t it = 0;
-        int64_t t = cid;
+        int64_t t = rq_get(rowq, bar_rq, 0);
         float C = 0.f;
-        if (t < p.T) C = stream_row(t, 0, false);
-        while (t < p.T) {
-            // park e_t in TMEM, stream row t + ncl (if any), then write row t from TMEM
-            const int64_t tn = t + ncl;
-            if (tn >= p.T) {  // last row: nothing to stream, park it all now
+        if (t >= 0) C = stream_row(t, 0, false);
+        while (t >= 0) {
+            // park e_t in TMEM, stream this CTA's next row (if any), then write row t from TMEM
+            const int64_t tn = rq_get(rowq, bar_rq, it + 1);
+            if (tn < 0) {  // last row: nothing to stream, park it all now
 #pragma unroll
                 for (int j = 0; j < NVT; ++j) tmem_st4(tm + 4 * j, r[j]);
             }
             if (dbg) pcc.lap(dph[2]);
             float Cn = 0.f;
-            if (tn < p.T) Cn = stream_row(tn, it + 1, true);
+            if (tn >= 0) Cn = stream_row(tn, it + 1, true);
             tmem_wait_st();  // e_t must be in TMEM before write_row reads it back
             write_row(t, it, C);
             C = Cn;
@@ -488,6 +511,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         if (dbg) {
             dph[5] = static_cast<unsigned long long>(clock64() - t_begin);
             for (int q = 0; q < 6; ++q) atomicAdd(p.dbg + q, dph[q]);
+            if (warp == 0) dbg_cta_end(p.dbg, it);
         }
     }
     tmem_fence_before();

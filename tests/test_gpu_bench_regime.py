@@ -282,3 +282,51 @@ def test_host_api_many_chunks_bit_equal_device(variant, agg):
                                                              scal, h_dl)
     compare(case, cfg, gr, ref, check_dlogits=False)
     check_dlogit_rows(case, cfg, gr, ref, sampled_rows(case.T, chunk, n_random=32))
+
+
+# ---------------------------------------------------------------------------
+# Row schedule: dynamic row claims (default) vs the static walk c, c + ncl, ...
+# (RF_ROW_SCHED=static, read once per process: a subprocess).  The per-row math and the
+# per-token partial rows do not depend on which cluster took a row, so the two are
+# bit-identical — scalars, token outputs and dlogits.
+# ---------------------------------------------------------------------------
+_SCHED_ARM = """
+import sys
+sys.path.insert(0, {root!r})
+import torch
+import paper_2510_11345_b200 as rf
+from tests.test_gpu_bench_regime import _sched_case
+cfg, pb = _sched_case({kl!r})
+r = rf.loss_and_grad(cfg, pb, kernel="ring")
+torch.save({{k: getattr(r, k).cpu() for k in _FIELDS}}, {out!r})
+print("arm ok")
+""".replace("_FIELDS", repr(["scalars", "dlogits", "token_logp", "token_ratio", "token_coef", "token_loss",
+                             "token_flags"]))
+
+
+def _sched_case(kl):
+    if kl:
+        case = make_pool_case(107, V=151936, R=96, T_min=16 * (SMS // 4) + 300, G=4, max_len=48, stale=0.2, kl=True)
+        cfg = _cfg("grpo", kl_weight=0.1)
+        return cfg, to_device_batch(case, with_ref=True, normalization=L.Normalization.global_token)
+    case = make_pool_case(108, V=151936, R=128, T_min=16 * (SMS // 2) + 500, G=8, max_len=96, stale=0.25, alpha=2)
+    cfg = _cfg("decoupled_ppo")
+    return cfg, to_device_batch(case, normalization=L.Normalization.global_token)
+
+
+@pytest.mark.parametrize("kl", [False, True])
+def test_row_schedule_static_bit_equal_dynamic(kl, tmp_path):
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "static.pt")
+    r = subprocess.run([sys.executable, "-c", _SCHED_ARM.format(root=root, kl=kl, out=out)],
+                       env={**os.environ, "RF_ROW_SCHED": "static"}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "arm ok" in r.stdout, r.stdout + r.stderr
+    static = torch.load(out)
+    cfg, pb = _sched_case(kl)
+    dyn = rf.loss_and_grad(cfg, pb, kernel="ring")
+    for k, v in static.items():
+        assert torch.equal(getattr(dyn, k).cpu(), v), k

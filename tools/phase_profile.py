@@ -35,7 +35,8 @@ pb = L.PackedBatch(logits=dw.pool, token_ids=dw.token_ids, seq_offsets=dw.seq_of
 cfg = config("grpo", kl_weight=0.1) if a.kl else config(a.variant)
 op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=min(65536, dw.T))
 lib = _abi.load_library()
-buf = np.zeros(16, dtype=np.uint64)
+NCTA_MAX = 1024
+buf = np.zeros(16 + 4 * NCTA_MAX, dtype=np.uint64)
 for rep in range(3):
     op.zero()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,7 +44,7 @@ for rep in range(3):
     op.run(pb, 0, op.chunk)
     ev1.record()
     torch.cuda.synchronize()
-    lib.rf_debug_counters(buf.ctypes.data, 16, 1)
+    lib.rf_debug_counters(buf.ctypes.data, buf.size, 1)
 ms = ev0.elapsed_time(ev1)
 names = ["cons.full_wait", "cons.stream", "cons.park", "cons.coef_wait", "cons.write", "cons.total",
          "scal.red_wait", "scal.peer_wait", "scal.math", "scal.total", "prod.empty_wait", "prod.total",
@@ -57,3 +58,20 @@ cons_warps = ncta * 12
 for i, n in enumerate(names):
     div = cons_warps if n.startswith("cons") else (ncta * 2 if n.startswith("scal") else ncta)
     print(f"{n:18s} {buf[i] / div / 1e3:10.1f} kcycles per warp   ({buf[i] / max(buf[5 if n.startswith('cons') else (9 if n.startswith('scal') else 11)], 1) * 100:5.1f}%)")
+# per-CTA consumer spans of the last launch: how much of the launch is the tail (CTAs finishing early
+# wait for the slowest group; static row assignment cannot rebalance)
+tt = buf[16:].reshape(-1, 4).astype(np.int64)
+tt = tt[(tt[:, 0] > 0) & (tt[:, 1] > 0)]
+if len(tt):
+    t0 = tt[:, 0].min()
+    end = (tt[:, 1] - t0) / 1e3
+    span = (tt[:, 1] - tt[:, 0]) / 1e3
+    q = np.percentile(end, [0, 10, 50, 90, 100])
+    print(f"CTA end times (us after the first CTA started), {len(tt)} CTAs: min {q[0]:.1f}  p10 {q[1]:.1f}  "
+          f"median {q[2]:.1f}  p90 {q[3]:.1f}  max {q[4]:.1f};  mean {end.mean():.1f} -> tail {(q[4] - end.mean()) / q[4] * 100:.1f}% of the launch")
+    print(f"CTA start skew: {(tt[:, 0].max() - t0) / 1e3:.1f} us; consumer spans: min {span.min():.1f}  max {span.max():.1f} us")
+    rate = tt[:, 3] / span  # rows per us
+    order = np.argsort(tt[:, 2])
+    print("per CTA by %smid: smid rows span_us us_per_row")
+    for i in order:
+        print(f"  {tt[i, 2]:4d} {tt[i, 3]:5d} {span[i]:9.1f} {span[i] / max(tt[i, 3], 1):7.3f}")
