@@ -179,7 +179,7 @@ int64_t partial_rows(const rf_batch* b) {
            rf::kFinalizeBlocks;
 }
 
-// Lag kernels: dynamic row claims (default) or the static cid + k·ncl walk (RF_ROW_SCHED=static, A/B).
+// Lag and stream kernels: dynamic row claims (default) or the static walk (RF_ROW_SCHED=static, A/B).
 bool dynamic_rows_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("RF_ROW_SCHED");
@@ -192,7 +192,7 @@ struct WsLayout {
     double* partials = nullptr;
     double *lse = nullptr, *lp = nullptr, *coef = nullptr, *klx = nullptr, *lseq = nullptr;
     void* xch = nullptr;  // exact-KL CTA-group exchange slots
-    unsigned int* row_ctr = nullptr;  // lag kernels: dynamic row counter
+    unsigned int* row_ctr = nullptr;  // dynamic row counters (lag kernel, or stats + write streams)
     size_t bytes = 0;
 };
 
@@ -451,6 +451,11 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
         if (kernel == RF_KERNEL_RING && !g.ok) return RF_ERR_UNSUPPORTED_LAYOUT;
         if (g.ok) {
             p.row_vecs = g.row_vecs;
+            // dynamic row claims (stats stream: counter 0, write stream: counter 1)
+            if (dynamic_rows_enabled()) {
+                p.row_ctr = ws.row_ctr;
+                if (cudaMemsetAsync(ws.row_ctr, 0, 2 * sizeof(unsigned int), s) != cudaSuccess) return RF_ERR_CUDA;
+            }
             if (rf::launch_stream_stats(p, ib, s) != cudaSuccess) return RF_ERR_CUDA;
         } else {
             if (rf::launch_generic(p, ib, ob, grid, s) != cudaSuccess) return RF_ERR_CUDA;
@@ -466,6 +471,7 @@ rf_status rf_loss_and_grad_ex(const rf_loss_config* c, const rf_batch* b, rf_out
             KParams q = p;
             q.mode = 2;
             q.token_coef = ws.coef;
+            if (q.row_ctr) q.row_ctr += 1;
             const cudaError_t e = g.ok ? rf::launch_stream_write(q, ib, ob, s) : rf::launch_generic(q, ib, ob, grid, s);
             if (e != cudaSuccess) return RF_ERR_CUDA;
             g_last_launches += 1;

@@ -46,6 +46,14 @@ int resident_grid(K kernel, int64_t T) {
 
 }  // namespace
 
+// The row after t for this CTA: claimed from the launch's counter (first rows are the block
+// ids, so the counter starts at gridDim.x), or the static walk t + gridDim.x without one.  A
+// CTA on a slower SM takes fewer rows instead of setting the launch's end.
+__device__ __forceinline__ int64_t next_row(const KParams& p, int64_t t) {
+    if (p.row_ctr == nullptr) return t + gridDim.x;
+    return static_cast<int64_t>(gridDim.x) + atomicAdd(p.row_ctr, 1u);
+}
+
 // Vectors in flight per thread (4 measured best of {4, 8}); resident CTAs per SM
 // the register allocation is bounded for: the read-only stats stream wants every
 // slot filled (8 CTAs, 32 registers: 6.1 vs 5.2 TB/s at 4), the write stream its
@@ -65,7 +73,10 @@ __global__ void __launch_bounds__(kStreamThreads, kWriteMinBlocks) stream_write_
     const int tail_vec = row_vecs - 1;
     const int tail_valid = p.V - tail_vec * EPV;
     const uint64_t L2 = pk2(kL2e, kL2e);
-    for (int64_t t = blockIdx.x; t < p.T; t += gridDim.x) {
+    __shared__ int64_t sRow[2];
+    int par = 0;
+    for (int64_t t = blockIdx.x; t < p.T; par ^= 1) {
+        if (tid == 0) sRow[par] = next_row(p, t);  // claimed while this row streams
         const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(p.logits) + row * p.row_stride * IES;
         uint8_t* dst = reinterpret_cast<uint8_t*>(p.dlogits) + t * p.dl_stride * OES;
@@ -143,6 +154,8 @@ __global__ void __launch_bounds__(kStreamThreads, kWriteMinBlocks) stream_write_
                 }
             }
         }
+        __syncthreads();  // the next row (double-buffered slot: one barrier per row)
+        t = sRow[par];
     }
 }
 
@@ -166,13 +179,15 @@ __global__ void __launch_bounds__(kStreamThreads, kStatsMinBlocks) stream_stats_
     const int tail_vec = row_vecs - 1;
     const int tail_valid = p.V - tail_vec * EPV;
     const uint64_t L2 = pk2(kL2e, kL2e);
+    __shared__ int64_t sRow[2];
     int par = 0;
-    for (int64_t t = blockIdx.x; t < p.T; t += gridDim.x, par ^= 1) {
+    for (int64_t t = blockIdx.x; t < p.T; par ^= 1) {
         const int64_t row = p.row_of_token ? static_cast<int64_t>(p.row_of_token[t]) : t;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(p.logits) + row * p.row_stride * IES;
         int32_t tok = 0;
         float x_tok = 0.0f;
-        if (tid == 0) {  // the sampled logit, loaded while the row streams
+        if (tid == 0) {  // the sampled logit, loaded while the row streams; the next row claimed
+            sRow[par] = next_row(p, t);
             tok = p.token_ids[t];
             if (tok >= 0 && tok < p.V) x_tok = load_logit(p.logits, row * p.row_stride + tok, IN_BF16);
         }
@@ -251,6 +266,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStatsMinBlocks) stream_stats_
             p.token_logp[t] = tok_ok ? static_cast<double>(x_tok) - lse : CUDART_NAN;
             if (!tok_ok) atomicOr(p.status, RF_DEVSTAT_TOKEN_OUT_OF_RANGE);
         }
+        t = sRow[par];  // written before this row's barrier
     }
 }
 

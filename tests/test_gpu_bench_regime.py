@@ -305,6 +305,10 @@ print("arm ok")
 
 
 def _sched_case(kl):
+    if kl == "seqprod":  # the sequence_product stats / write streams (up to 1,184 CTAs, ~4 rows each)
+        case = make_pool_case(109, V=32000, R=256, T_min=4 * 8 * SMS + 300, G=8, max_len=160, stale=0.25, alpha=4)
+        cfg = _cfg("tis", aggregation="sequence_product")
+        return cfg, to_device_batch(case, normalization=L.Normalization.seq_then_batch)
     if kl:
         case = make_pool_case(107, V=151936, R=96, T_min=16 * (SMS // 4) + 300, G=4, max_len=48, stale=0.2, kl=True)
         cfg = _cfg("grpo", kl_weight=0.1)
@@ -314,7 +318,7 @@ def _sched_case(kl):
     return cfg, to_device_batch(case, normalization=L.Normalization.global_token)
 
 
-@pytest.mark.parametrize("kl", [False, True])
+@pytest.mark.parametrize("kl", [False, True, "seqprod"])
 def test_row_schedule_static_bit_equal_dynamic(kl, tmp_path):
     import os
     import subprocess
