@@ -517,7 +517,8 @@ __device__ __forceinline__ TokenPre token_pre(const KParams& p, int64_t t, int64
 
 // The lp-dependent half (losses.cpp:264-320).  On the scalar lane's critical path:
 // with VARIANT fixed, no other variant's work (e.g. decoupled_ppo's second exp) is
-// evaluated and discarded.
+// evaluated and discarded; kNotDecoupled = any variant but decoupled_ppo (runtime).
+constexpr int kNotDecoupled = -2;
 template <int VARIANT = -1>
 __device__ __forceinline__ TokenResult token_post(const KParams& p, const TokenPre& q, double lp) {
     TokenResult o;
@@ -526,7 +527,7 @@ __device__ __forceinline__ TokenResult token_post(const KParams& p, const TokenP
     o.ratio = r;
     if (!isfinite(r)) o.flags |= RF_FLAG_NONFINITE;
     const int variant = VARIANT >= 0 ? VARIANT : p.variant;
-    const double tp = (variant == RF_DECOUPLED_PPO) ? exp(lp - q.lq) : 0.0;
+    const double tp = (VARIANT != kNotDecoupled && variant == RF_DECOUPLED_PPO) ? exp(lp - q.lq) : 0.0;
     double value, gw;
     variant_math<VARIANT>(p, r, q.A, q.po, tp, lp, value, gw, o.flags);
     const double sm = __dmul_rn(q.scale, q.m);

@@ -263,7 +263,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     tr.flags = RF_FLAG_NONFINITE | RF_FLAG_ZERO_COEF;
                 } else {
                     lp = static_cast<double>(x_tok) - lse;
-                    tr = token_post(p, pre, lp);
+                    // uniform branch: the decoupled ratio's exp only where it is used
+                    tr = (p.variant == RF_DECOUPLED_PPO) ? token_post<RF_DECOUPLED_PPO>(p, pre, lp)
+                                                         : token_post<kNotDecoupled>(p, pre, lp);
                     if (tr.flags & RF_FLAG_NONFINITE) atomicOr(p.status, RF_DEVSTAT_NONFINITE_RATIO);
                 }
                 bc->k = tr.k;
