@@ -202,6 +202,9 @@ rf_status rf_loss_variant_from_name(const char* name, int32_t* variant_out);
 const char* rf_status_string(rf_status status);
 
 /* ---- device API (stream-ordered; all buffers device-resident) ---- */
+/* Scratch for one call: 64 bytes per token (one fp64 partial-scalar row per token,
+ * reduced in a fixed order), the row counters, and for sequence_product / exact KL
+ * their per-token and exchange arrays. */
 size_t rf_workspace_bytes(const rf_loss_config* cfg, const rf_batch* batch);
 
 /* K1: GRPO group-relative advantages (grpo_advantages, losses.cpp:41-60), one
