@@ -18,7 +18,9 @@
 //   write:  dlogit_v = p_v·(kc·(d_v - D) - k) (+ k at the sampled token)
 //                    = e_v·(A + B·d_v),  A = -f·(k + kc·D),  B = f·kc,  f = 2^(C - lse·log2e)
 //
-// e and d are parked in TMEM as f16 (2·NVT·4 columns per thread).
+// e and d are parked in TMEM as f16 (2·NVT·4 columns per thread).  Rows are claimed
+// at run time (the group's rank 0 posts them to the group's claim ring in L2, or, in a
+// hardware cluster, into every rank's shared-memory row queue: rf_lag_common.cuh).
 #include <cuda_runtime.h>
 #include <math_constants.h>
 

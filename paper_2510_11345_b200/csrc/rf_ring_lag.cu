@@ -16,9 +16,12 @@
 // next to the register file; the scalar warps (DSMEM cluster exchange + fp64
 // surrogate math, losses.cpp:264-320) have a whole row of streaming to finish.
 // One CTA per SM: 12 consumer warps (152 registers via setmaxnreg) + one support
-// warpgroup (TMA producer, two scalar warps for even/odd rows, one idle warp);
-// 2-CTA clusters for the Qwen3 vocabulary.  The alternatives measured against
-// each design choice are logged in profiles/r01_ab/ab_log.txt.
+// warpgroup (TMA producer, two scalar warps for even/odd rows, one idle warp).
+// Rows are claimed at run time from a per-launch counter by each cluster's rank-0
+// producer and handed to every role through a shared-memory row queue
+// (rf_lag_common.cuh), so faster SM pairs take more rows.  2-CTA clusters for the
+// Qwen3 vocabulary.  The alternatives measured against each design choice are
+// logged in profiles/r01_ab/ab_log.txt and profiles/r02_ab/.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 

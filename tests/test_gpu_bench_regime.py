@@ -1,7 +1,8 @@
 """GPU parity in the regime the benchmark runs: many rows per CTA / cluster.
 
-The persistent kernels walk rows c, c + ncl, c + 2·ncl, … per CTA (or cluster),
-so everything that only exists from the second row on — the lag kernel's
+The persistent kernels walk many rows per CTA (or cluster) — claimed from a per-launch
+counter, or c, c + ncl, c + 2·ncl, … with RF_ROW_SCHED=static — so everything that only
+exists from the second row on — the lag kernel's
 row-to-row TMEM parking, the even/odd scalar warps, the bar_red/bar_bc phase
 alternation, the xslot[row & 3] exchange slots, ring-slot phase flips, the
 stream kernels' double-buffered per-row slots, the exact-KL CTA groups' L2
