@@ -191,9 +191,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         // --------------------------------- scalar ---------------------------------
         // Two scalar warps: warp NCW+1 owns the even rows of this cluster, NCW+2 the
         // odd ones (row parity == buffer parity), so each has two rows of
-        // streaming to finish its exchange + fp64 math.  Lane 0 does the work (a
-        // 32-lane shuffle-tree combine measured no faster).
-        if (lane == 0) {
+        // streaming to finish its exchange + fp64 math.  The whole warp combines the
+        // consumer warps' partials (one per lane, shuffle trees); lane 0 alone runs the
+        // exchange, the token math and the broadcast.
+        {
             const uint32_t which = static_cast<uint32_t>(warp - NCW - 1);
             unsigned long long d_red = 0, d_x = 0, d_math = 0, d_post = 0;
             PhaseClock pc;
@@ -213,16 +214,18 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
                 support_wait(bar_red + 8 * par, ph);
                 if (kPhaseCounters && p.dbg) pc.lap(d_red);
-                if (kChecked)
-                    for (int w = 0; w < NCW; ++w) rf_check(red_tag[par * NCW + w] == t);
-                // combine the consumer warps' partials, sequential in warp order
-                float Mw = -CUDART_INF_F;
-                for (int w = 0; w < NCW; ++w) Mw = fmaxf(Mw, redM[par * NCW + w]);
-                double Sw = 0.0;
-                for (int w = 0; w < NCW; ++w) {
-                    const double sw = redS[par * NCW + w];
-                    if (sw != 0.0) Sw += sw * combine_factor(redM[par * NCW + w], Mw);
-                }
+                if (kChecked && lane < NCW) rf_check(red_tag[par * NCW + lane] == t);
+                // combine the consumer warps' partials: lane w holds warp w's, fixed butterfly
+                // trees (lane 0's result is the one used; the same on every launch)
+                const float m_l = lane < NCW ? redM[par * NCW + lane] : -CUDART_INF_F;
+                const double s_l = lane < NCW ? redS[par * NCW + lane] : 0.0;
+                float Mw = m_l;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
+                double Sw = (s_l != 0.0) ? s_l * combine_factor(m_l, Mw) : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) Sw += __shfl_xor_sync(0xffffffffu, Sw, o);
+                if (lane == 0) {
                 double Mc = static_cast<double>(Mw), Sc = Sw;
                 if (csize > 1) {
                     // push (S, M) to every peer's slot [row % 4][my rank], publish it with a
@@ -289,8 +292,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
                     Partials::store_token(p.partials + static_cast<size_t>(t) * RF_NUM_SCALARS, tr, 0.0);
                 }
                 if (kPhaseCounters && p.dbg) pc.lap(d_math);
+                }  // lane 0
+                __syncwarp();
             }
-            if (kPhaseCounters && p.dbg) {
+            if (kPhaseCounters && p.dbg && lane == 0) {
                 atomicAdd(p.dbg + 6, d_red);
                 atomicAdd(p.dbg + 7, d_x);
                 atomicAdd(p.dbg + 8, d_math);
