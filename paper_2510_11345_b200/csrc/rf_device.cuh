@@ -94,18 +94,26 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-// Profiling build: per-CTA consumer {start ns, end ns (%globaltimer), %smid, rows} in
-// dbg[kDbgCtaTimes + 4·cta + {0..3}].
+// Profiling build: per-CTA record of consumer warp 0, lane 0 in dbg[kDbgCtaTimes + 8·cta + i]:
+// {start ns, end ns (%globaltimer), %smid, rows, full-wait, stream, coef-wait, write cycles}.
 constexpr int kDbgCtaTimes = 16;
-constexpr int kDbgWords = kDbgCtaTimes + 4 * 1024;
-__device__ __forceinline__ void dbg_cta_end(unsigned long long* dbg, uint32_t rows) {
+constexpr int kDbgCtaWords = 8;
+constexpr int kDbgWords = kDbgCtaTimes + kDbgCtaWords * 1024;
+__device__ __forceinline__ void dbg_cta_begin(unsigned long long* dbg) {
+    if (blockIdx.x < 1024) dbg[kDbgCtaTimes + kDbgCtaWords * blockIdx.x] = global_ns();
+}
+__device__ __forceinline__ void dbg_cta_end(unsigned long long* dbg, uint32_t rows, const unsigned long long* dph) {
     if (blockIdx.x >= 1024) return;
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    unsigned long long* w = dbg + kDbgCtaTimes + 4 * blockIdx.x;
+    unsigned long long* w = dbg + kDbgCtaTimes + kDbgCtaWords * blockIdx.x;
     w[1] = global_ns();
     w[2] = smid;
     w[3] = rows;
+    w[4] = dph[0];
+    w[5] = dph[1];
+    w[6] = dph[3];
+    w[7] = dph[4];
 }
 
 // Debug phase timer: accumulates clock64 deltas into a per-thread slot array.

@@ -571,7 +571,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         pcc.start();
         const long long t_begin = pcc.t;
         const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
-        if (dbg && warp == 0 && blockIdx.x < 1024) p.dbg[kDbgCtaTimes + 4 * blockIdx.x] = global_ns();
+        if (dbg && warp == 0) dbg_cta_begin(p.dbg);
 
         // copy-in (parking the previous row's e and d chunk by chunk), max, sweep, reduce
         auto stream_row = [&](int64_t t_row, uint32_t row_iter, bool park_prev) -> float {
@@ -771,7 +771,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_kl_kernel(const __grid
         if (dbg) {
             dph[5] = static_cast<unsigned long long>(clock64() - t_begin);
             for (int q = 0; q < 6; ++q) atomicAdd(p.dbg + q, dph[q]);
-            if (warp == 0) dbg_cta_end(p.dbg, it);
+            if (warp == 0) dbg_cta_end(p.dbg, it, dph);
         }
     }
     tmem_fence_before();

@@ -338,7 +338,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         pcc.start();
         const long long t_begin = pcc.t;
         const bool dbg = kPhaseCounters && p.dbg != nullptr && lane == 0;
-        if (dbg && warp == 0 && blockIdx.x < 1024) p.dbg[kDbgCtaTimes + 4 * blockIdx.x] = global_ns();
+        if (dbg && warp == 0) dbg_cta_begin(p.dbg);
 
         // copy-in + max + exp sweep + CTA reduction of row t into r[]; returns C_t.
         auto stream_row = [&](int64_t t_row, uint32_t row_iter, bool park_prev) -> float {
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) ring_lag_kernel(const __gri
         if (dbg) {
             dph[5] = static_cast<unsigned long long>(clock64() - t_begin);
             for (int q = 0; q < 6; ++q) atomicAdd(p.dbg + q, dph[q]);
-            if (warp == 0) dbg_cta_end(p.dbg, it);
+            if (warp == 0) dbg_cta_end(p.dbg, it, dph);
         }
     }
     tmem_fence_before();

@@ -115,12 +115,23 @@ def test_rows_segment_sum_is_the_in_order_fp64_sum(dtype):
     assert (got[:, W:] == 3.0).all()  # nothing written past the width
 
 
-def test_exact_kl_graph_replay_equals_eager():
-    """the CTA-group exchange slots are guarded by sequence words; captured
-    into a CUDA graph and replayed on new logits, every replay must see fresh slots."""
-    case = make_pool_case(43, V=151936, R=48, T_min=700, G=4, max_len=48, stale=0.2, kl=True)
-    cfg = config("grpo", kl_weight=0.1, engine_mismatch_cap=2.0)
-    pb = to_device_batch(case, with_ref=True, normalization=L.Normalization.global_token)
+@pytest.mark.parametrize("path", ["exact_kl", "lag", "seqprod"])
+def test_graph_replay_equals_eager(path):
+    """the CTA-group exchange slots are guarded by sequence words, and every
+    persistent kernel claims its rows from a per-launch counter; captured into a CUDA
+    graph and replayed on new logits, every replay must see fresh slots and counters."""
+    norm = L.Normalization.global_token
+    if path == "exact_kl":
+        case = make_pool_case(43, V=151936, R=48, T_min=700, G=4, max_len=48, stale=0.2, kl=True)
+        cfg = config("grpo", kl_weight=0.1, engine_mismatch_cap=2.0)
+    elif path == "lag":
+        case = make_pool_case(44, V=151936, R=48, T_min=700, G=4, max_len=48, stale=0.2)
+        cfg = config("decoupled_ppo", engine_mismatch_cap=2.0)
+    else:
+        case = make_pool_case(45, V=32000, R=64, T_min=2600, G=4, max_len=96, stale=0.2)
+        cfg = config("tis", aggregation="sequence_product")
+        norm = L.Normalization.seq_then_batch
+    pb = to_device_batch(case, with_ref=(path == "exact_kl"), normalization=norm)
     T = pb.num_tokens
     op = rf.OffPolicyLoss(cfg, pb, kernel="ring")
     s = torch.cuda.Stream()
@@ -148,7 +159,7 @@ def test_exact_kl_graph_replay_equals_eager():
         assert torch.equal(op.scalars, eager.scalars), rep
     # and the last replay against the oracle on the replayed logits
     case.logits = pb.logits.double().cpu().numpy()
-    compare(case, cfg, op, run_oracle(case, cfg, normalization=1, want_dlogits=False), check_dlogits=False)
+    compare(case, cfg, op, run_oracle(case, cfg, normalization=int(norm), want_dlogits=False), check_dlogits=False)
 
 
 def test_host_api_leaves_default_mempool_alone():

@@ -36,7 +36,7 @@ cfg = config("grpo", kl_weight=0.1) if a.kl else config(a.variant)
 op = rf.OffPolicyLoss(cfg, pb, chunk_tokens=min(65536, dw.T))
 lib = _abi.load_library()
 NCTA_MAX = 1024
-buf = np.zeros(16 + 4 * NCTA_MAX, dtype=np.uint64)
+buf = np.zeros(16 + 8 * NCTA_MAX, dtype=np.uint64)
 for rep in range(3):
     op.zero()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -60,7 +60,7 @@ for i, n in enumerate(names):
     print(f"{n:18s} {buf[i] / div / 1e3:10.1f} kcycles per warp   ({buf[i] / max(buf[5 if n.startswith('cons') else (9 if n.startswith('scal') else 11)], 1) * 100:5.1f}%)")
 # per-CTA consumer spans of the last launch: how much of the launch is the tail (CTAs finishing early
 # wait for the slowest group; static row assignment cannot rebalance)
-tt = buf[16:].reshape(-1, 4).astype(np.int64)
+tt = buf[16:].reshape(-1, 8).astype(np.int64)
 tt = tt[(tt[:, 0] > 0) & (tt[:, 1] > 0)]
 if len(tt):
     t0 = tt[:, 0].min()
@@ -70,8 +70,10 @@ if len(tt):
     print(f"CTA end times (us after the first CTA started), {len(tt)} CTAs: min {q[0]:.1f}  p10 {q[1]:.1f}  "
           f"median {q[2]:.1f}  p90 {q[3]:.1f}  max {q[4]:.1f};  mean {end.mean():.1f} -> tail {(q[4] - end.mean()) / q[4] * 100:.1f}% of the launch")
     print(f"CTA start skew: {(tt[:, 0].max() - t0) / 1e3:.1f} us; consumer spans: min {span.min():.1f}  max {span.max():.1f} us")
-    rate = tt[:, 3] / span  # rows per us
     order = np.argsort(tt[:, 2])
-    print("per CTA by %smid: smid rows span_us us_per_row")
+    tot = tt[:, 4:8].sum(axis=1).clip(min=1)
+    print("per CTA by %smid (consumer warp 0): smid rows span_us us_per_row  full_wait% stream% coef_wait% write%")
     for i in order:
-        print(f"  {tt[i, 2]:4d} {tt[i, 3]:5d} {span[i]:9.1f} {span[i] / max(tt[i, 3], 1):7.3f}")
+        f = tt[i, 4:8] / tot[i] * 100
+        print(f"  {tt[i, 2]:4d} {tt[i, 3]:5d} {span[i]:9.1f} {span[i] / max(tt[i, 3], 1):7.3f}   "
+              f"{f[0]:5.1f} {f[1]:5.1f} {f[2]:5.1f} {f[3]:5.1f}")
